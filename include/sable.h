@@ -1,0 +1,236 @@
+/*
+ * sable.h -- C-ABI of libsable.so, the B200 (sm_100a) VBR SpMV hot path of
+ * SABLE (arXiv 2407.00829, "Staging Blocked Evaluation over Structured Sparse
+ * Matrices").  Citations "PAPER.md:L" are lines of the paper's LaTeX source;
+ * readings R1..R18 are listed in DESIGN.md ("Readings of the paper").
+ *
+ * The boundary (BASELINE.json north_star s3): sable_vbr_create takes the VBR
+ * indirection arrays rpntr / cpntr / bpntr / bindx / indx / val (Fig. 2,
+ * PAPER.md:221-228; "SABLE assumes that the sparse matrix is already stored
+ * in the VBR format and takes several storage format indirection arrays as
+ * input") plus the delta threshold ("delta-dense ... the
+ * percentage of non-zero elements is at least delta %"), runs
+ * the GPU inspector, and returns a handle; sable_spmv computes y = A x
+ * with the dense tiles / CSR remainder split of VBR-C (Fig. 3,
+ * PAPER.md:271-347); sable_destroy frees the handle.
+ *
+ * Conventions for every entry point:
+ *   - plain C types and pointers only; no exceptions cross the ABI; every call
+ *     returns a sable_status; the text of the last failure on the calling
+ *     thread is available from sable_last_error().
+ *   - "device pointer" = CUDA device memory of the current device (e.g. the
+ *     data_ptr() of a torch CUDA tensor); "host pointer" = ordinary or pinned
+ *     host memory.
+ *   - cuda_stream is a cudaStream_t passed as void* (NULL = legacy default).
+ *   - Indices are 0-based.  Sizes are element counts unless named *_bytes.
+ */
+#ifndef SABLE_H_
+#define SABLE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SABLE_ABI_VERSION 1
+
+typedef struct sable_handle sable_handle;
+
+typedef enum {
+  SABLE_OK = 0,
+  SABLE_E_INVALID_ARG = 1, /* NULL pointer, delta > 101, bad enum, bad shard   */
+  SABLE_E_FORMAT = 2,      /* a VBR / remainder invariant is broken; the last
+                              error names the array and the first bad index    */
+  SABLE_E_DIM = 3,         /* sizes disagree (e.g. iterate on a non-square A)  */
+  SABLE_E_DUPLICATE = 4,   /* the same (i,j) non-zero in val and the remainder */
+  SABLE_E_OOM = 5,         /* device or host allocation failed                 */
+  SABLE_E_CUDA = 6,        /* a CUDA runtime error (text in sable_last_error)  */
+  SABLE_E_NCCL = 7,        /* an NCCL error                                    */
+  SABLE_E_UNSUPPORTED = 8  /* outside the supported limits (see below)         */
+} sable_status;
+
+typedef enum { SABLE_F32 = 0, SABLE_F64 = 1 } sable_dtype;
+typedef enum { SABLE_MEM_HOST = 0, SABLE_MEM_DEVICE = 1 } sable_mem;
+
+/*
+ * A matrix in VBR form (Fig. 2) with an optional CSR
+ * remainder (Fig. 3 indptr/indices/csr_val).
+ *
+ * Layout and invariants (violations -> SABLE_E_FORMAT, naming array + index):
+ *   rpntr[nbrows+1] int32: 0 = rpntr[0] < rpntr[1] < ... < rpntr[nbrows] = nrows
+ *                          ("starting index of each block row", Fig. 2 Rpntr)
+ *   cpntr[nbcols+1] int32: the same for columns (Fig. 2 Cpntr)
+ *   bpntr[nbrows+1] int64: the stored blocks of block row a are
+ *                          [bpntr[a], bpntr[a+1]); bpntr[0]=0, non-decreasing,
+ *                          bpntr[nbrows] = nblocks.  The paper's pair is
+ *                          Bpntrb[a] = bpntr[a] (or -1 if empty), Bpntre[a] =
+ *                          bpntr[a+1] (reading R9).
+ *   bindx[nblocks]  int32: block column of each block, in [0, nbcols), strictly
+ *                          increasing within a block row (Fig. 2 Bindx; R10)
+ *   indx[nblocks+1] int64: indx[0]=0, indx[k+1]-indx[k] = h*w of block k,
+ *                          indx[nblocks] = val_len ("inclusive of the length
+ *                          of the Val array")
+ *   val[val_len]    dtype: block k's h x w values column-major:
+ *                          A(r0+r, c0+c) = val[indx[k] + c*h + r]
+ *                          (reading R8).  Stored zeros
+ *                          (+0 or -0) are zero fill, not non-zeros (R4).
+ *   rem_indptr[nrows+1] int64, rem_indices[rem_nnz] int32, rem_val[rem_nnz]:
+ *                          optional CSR remainder (all three NULL and
+ *                          rem_nnz = 0 for none); columns strictly increasing
+ *                          within a row.  A position that is non-zero in both
+ *                          val and the remainder -> SABLE_E_DUPLICATE.
+ * The matrix is the union of both sources.  The inspector's partition does not
+ * depend on how the caller splits non-zeros between them (reading R5).
+ * nblocks, val_len and rem_nnz are passed explicitly so that sizes are known
+ * without reading device memory; they are checked against the arrays.
+ * Limits (-> SABLE_E_UNSUPPORTED): nrows, ncols < 2^31; nblocks + rem_nnz
+ * < 2^31; the local remainder after classification < 2^31 entries.
+ */
+typedef struct {
+  int64_t nrows, ncols;
+  int32_t nbrows, nbcols;
+  int64_t nblocks;  /* = bpntr[nbrows]      */
+  int64_t val_len;  /* = indx[nblocks]      */
+  int64_t rem_nnz;  /* = rem_indptr[nrows]  */
+  int32_t dtype;    /* sable_dtype of val, rem_val, x and y */
+  int32_t mem;      /* sable_mem: where ALL arrays of this descriptor live */
+  const int32_t* rpntr;
+  const int32_t* cpntr;
+  const int64_t* bpntr;
+  const int32_t* bindx;
+  const int64_t* indx;
+  const void* val;
+  const int64_t* rem_indptr;
+  const int32_t* rem_indices;
+  const void* rem_val;
+} sable_vbr_desc;
+
+/* Row sharding for multi-GPU (BASELINE.json north_star s7): the handle of
+ * rank r of world P owns a contiguous block-row range chosen by
+ * sable_shard_bounds over per-block-row stored-entry weights.  NULL or
+ * {0, 1} = the whole matrix. */
+typedef struct {
+  int32_t rank, world;
+} sable_shard;
+
+typedef struct {
+  int64_t nrows, ncols;
+  int32_t nbrows, nbcols;
+  int32_t br_begin, br_end;   /* local block rows [br_begin, br_end)          */
+  int64_t row_begin, row_end; /* local rows: y has row_end - row_begin entries */
+  int64_t nnz;                /* true non-zeros in the local rows             */
+  int64_t n_cells;            /* local candidate cells (cnt >= 1)             */
+  int64_t cell_base;          /* candidate cells in block rows < br_begin     */
+  int64_t n_dense;            /* local delta-dense cells (tiles)              */
+  int64_t tile_elems;         /* sum of their areas (zero fill included)      */
+  int64_t rem_nnz;            /* local remainder non-zeros                    */
+  int64_t n_dense_global;     /* tiles over the whole matrix                  */
+  int64_t bytes_alg;          /* algorithmic bytes per sable_spmv */
+  int64_t n_groups, n_items;  /* executor work decomposition                  */
+  int32_t dtype;
+  int32_t delta;
+  int32_t suitable;           /* >= 1 dense tile in the matrix */
+  int32_t world, rank;
+  double inspect_ms;          /* wall time of sable_vbr_create's inspector    */
+} sable_info;
+
+/* Caller-allocated HOST buffers for sable_export_partition, sized from
+ * sable_info of the same handle (the canonical export of DESIGN.md, equal
+ * byte for byte to the oracle's, restricted to the local block rows):
+ *   cell_br, cell_bc [n_cells] int32; cell_cnt [n_cells] int64;
+ *   cell_dense [n_cells] uint8      -- candidate cells in (br, bc) order
+ *   tile_off [n_dense+1] int64      -- dense-only offsets (reading R7)
+ *   tile_val [tile_elems] dtype     -- column-major, zero-filled tiles
+ *   ublocks [n_cells-n_dense] int64 -- ordinals of non-dense cells, relative
+ *                                      to the first local cell (add cell_base
+ *                                      for global ordinals; Fig. 3 ublocks)
+ *   rem_indptr [row_end-row_begin+1] int64, rem_indices [rem_nnz] int32,
+ *   rem_val [rem_nnz] dtype         -- the remainder, row-major (reading R6)
+ * Any pointer may be NULL to skip that array. */
+typedef struct {
+  int32_t* cell_br;
+  int32_t* cell_bc;
+  int64_t* cell_cnt;
+  uint8_t* cell_dense;
+  int64_t* tile_off;
+  void* tile_val;
+  int64_t* ublocks;
+  int64_t* rem_indptr;
+  int32_t* rem_indices;
+  void* rem_val;
+} sable_partition_host;
+
+/* Inspect a VBR matrix on the current CUDA device (north_star (1)): validate
+ * the arrays (SPEC-style invariants above), count the non-zeros of every grid
+ * cell from val and the remainder, classify each candidate cell as
+ * delta-dense (100*cnt >= delta*h*w in int64, readings R1,
+ * R3), pack the dense tiles, assemble the CSR remainder, and plan the
+ * executor work.  delta_pct in [0, 101] (101 = nothing dense).
+ * All inputs are copied; the call synchronises cuda_stream before returning,
+ * so the caller may free its arrays.  The handle owns its device memory.
+ * On any error *out is set to NULL and nothing is leaked. */
+sable_status sable_vbr_create(const sable_vbr_desc* desc, uint32_t delta_pct,
+                              const sable_shard* shard, void* cuda_stream,
+                              sable_handle** out);
+
+/* y = A x for the handle's local rows.  x: device pointer to
+ * ncols dtype values (the full x); y: device pointer to row_end-row_begin
+ * values, written once each (no accumulation into y).  x and y must not
+ * alias.  Asynchronous on cuda_stream: no host synchronisation, no
+ * allocation.  A handle must not run two calls concurrently (split-row
+ * scratch).  x must be finite (reading R13). */
+sable_status sable_spmv(sable_handle* h, const void* x, void* y, void* cuda_stream);
+
+/* The same product with HOST buffers (end-to-end path): copies x host->device
+ * into handle-owned memory, runs sable_spmv, copies y device->host, and
+ * synchronises cuda_stream.  Pinned host memory gives full copy bandwidth. */
+sable_status sable_spmv_host(sable_handle* h, const void* x_host, void* y_host,
+                             void* cuda_stream);
+
+/* Free the handle (NULL is a no-op).  Synchronises the device first. */
+sable_status sable_destroy(sable_handle* h);
+
+sable_status sable_get_info(const sable_handle* h, sable_info* info);
+
+/* Copy the canonical partition of the local block rows to host buffers
+ * (see sable_partition_host).  Synchronous. */
+sable_status sable_export_partition(const sable_handle* h, const sable_partition_host* out);
+
+/* Host-only (no GPU needed): block-row shard boundaries for `world` ranks.
+ * weights[nbrows] >= 0 (stored entries streamed per block row: tile areas +
+ * remainder non-zeros, reading of north_star s7 in DESIGN.md); bounds[world+1]
+ * receives 0 = b0 <= b1 <= ... <= b_world = nbrows with boundary k = the
+ * first a whose prefix weight reaches k * total / world. */
+sable_status sable_shard_bounds(const int64_t* weights, int32_t nbrows, int32_t world,
+                                int32_t* bounds);
+
+/* ---- multi-GPU exchange (north_star s7: y slices all-gathered with NCCL) */
+
+/* Write a fresh ncclUniqueId (128 bytes) to out; rank 0 calls this and
+ * broadcasts the bytes (e.g. over torch.distributed). */
+sable_status sable_nccl_unique_id(void* out128);
+
+/* Create the handle's NCCL communicator (rank/world from the create shard). */
+sable_status sable_comm_init(sable_handle* h, const void* id128);
+
+/* One exchange step: x_next[row_begin:row_end] = (A x)[local rows], then
+ * every rank's slice is all-gathered into x_next (ncols entries) on every
+ * rank.  Requires a square matrix (SABLE_E_DIM) and sable_comm_init when
+ * world > 1.  x_full and x_next_full are device pointers, not aliased. */
+sable_status sable_spmv_allgather(sable_handle* h, const void* x_full, void* x_next_full,
+                                  void* cuda_stream);
+
+/* iters exchange steps ping-ponging x_a -> x_b -> x_a ...; *result_in_b = 1
+ * if the final x is in x_b.  Asynchronous on cuda_stream. */
+sable_status sable_spmv_iterate(sable_handle* h, void* x_a, void* x_b, int32_t iters,
+                                void* cuda_stream, int32_t* result_in_b);
+
+const char* sable_status_string(sable_status s);
+const char* sable_last_error(void); /* thread-local; "" if none */
+int32_t sable_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SABLE_H_ */

@@ -1,0 +1,313 @@
+"""Thin ctypes binding of libsable.so (include/sable.h) -- argument
+marshalling only.  Every step of the hot path runs in the library's CUDA
+kernels; PyTorch is used only for device memory, streams and process groups.
+
+There is no fallback: if libsable.so is missing or does not load, importing
+this module raises ImportError (build it with ``python -m
+paper_2407_00829_b200.build`` or ``__graft_entry__.build()``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsable.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libsable.so not built at {LIB_PATH}; run __graft_entry__.build()")
+try:
+    _lib = C.CDLL(LIB_PATH)
+except OSError as e:  # pragma: no cover - loud failure, no CPU fallback
+    raise ImportError(f"cannot load {LIB_PATH}: {e}") from e
+
+SABLE_OK, SABLE_E_INVALID_ARG, SABLE_E_FORMAT, SABLE_E_DIM, SABLE_E_DUPLICATE, \
+    SABLE_E_OOM, SABLE_E_CUDA, SABLE_E_NCCL, SABLE_E_UNSUPPORTED = range(9)
+SABLE_F32, SABLE_F64 = 0, 1
+SABLE_MEM_HOST, SABLE_MEM_DEVICE = 0, 1
+
+#: every symbol declared in include/sable.h
+EXPORTS = ("sable_vbr_create", "sable_spmv", "sable_spmv_host", "sable_destroy",
+           "sable_get_info", "sable_export_partition", "sable_shard_bounds",
+           "sable_nccl_unique_id", "sable_comm_init", "sable_spmv_allgather",
+           "sable_spmv_iterate", "sable_status_string", "sable_last_error",
+           "sable_abi_version")
+
+
+class sable_vbr_desc(C.Structure):
+    _fields_ = [("nrows", C.c_int64), ("ncols", C.c_int64),
+                ("nbrows", C.c_int32), ("nbcols", C.c_int32),
+                ("nblocks", C.c_int64), ("val_len", C.c_int64), ("rem_nnz", C.c_int64),
+                ("dtype", C.c_int32), ("mem", C.c_int32),
+                ("rpntr", C.c_void_p), ("cpntr", C.c_void_p), ("bpntr", C.c_void_p),
+                ("bindx", C.c_void_p), ("indx", C.c_void_p), ("val", C.c_void_p),
+                ("rem_indptr", C.c_void_p), ("rem_indices", C.c_void_p),
+                ("rem_val", C.c_void_p)]
+
+
+class sable_shard(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32)]
+
+
+class sable_info(C.Structure):
+    _fields_ = [("nrows", C.c_int64), ("ncols", C.c_int64),
+                ("nbrows", C.c_int32), ("nbcols", C.c_int32),
+                ("br_begin", C.c_int32), ("br_end", C.c_int32),
+                ("row_begin", C.c_int64), ("row_end", C.c_int64),
+                ("nnz", C.c_int64), ("n_cells", C.c_int64), ("cell_base", C.c_int64),
+                ("n_dense", C.c_int64), ("tile_elems", C.c_int64), ("rem_nnz", C.c_int64),
+                ("n_dense_global", C.c_int64), ("bytes_alg", C.c_int64),
+                ("n_groups", C.c_int64), ("n_items", C.c_int64),
+                ("dtype", C.c_int32), ("delta", C.c_int32), ("suitable", C.c_int32),
+                ("world", C.c_int32), ("rank", C.c_int32), ("inspect_ms", C.c_double)]
+
+
+class sable_partition_host(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("cell_br", "cell_bc", "cell_cnt", "cell_dense",
+                                           "tile_off", "tile_val", "ublocks", "rem_indptr",
+                                           "rem_indices", "rem_val")]
+
+
+_H = C.c_void_p
+_P = C.c_void_p
+_sig = {
+    "sable_vbr_create": [C.POINTER(sable_vbr_desc), C.c_uint32, C.POINTER(sable_shard), _P,
+                         C.POINTER(_H)],
+    "sable_spmv": [_H, _P, _P, _P],
+    "sable_spmv_host": [_H, _P, _P, _P],
+    "sable_destroy": [_H],
+    "sable_get_info": [_H, C.POINTER(sable_info)],
+    "sable_export_partition": [_H, C.POINTER(sable_partition_host)],
+    "sable_shard_bounds": [_P, C.c_int32, C.c_int32, _P],
+    "sable_nccl_unique_id": [_P],
+    "sable_comm_init": [_H, _P],
+    "sable_spmv_allgather": [_H, _P, _P, _P],
+    "sable_spmv_iterate": [_H, _P, _P, C.c_int32, _P, C.POINTER(C.c_int32)],
+}
+for _name, _args in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = C.c_int
+_lib.sable_status_string.argtypes = [C.c_int]
+_lib.sable_status_string.restype = C.c_char_p
+_lib.sable_last_error.argtypes = []
+_lib.sable_last_error.restype = C.c_char_p
+_lib.sable_abi_version.argtypes = []
+_lib.sable_abi_version.restype = C.c_int32
+
+
+class SableError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _lib.sable_last_error().decode()
+        super().__init__(f"{where}: {_lib.sable_status_string(status).decode()}: {msg}")
+
+
+def _check(status: int, where: str):
+    if status != SABLE_OK:
+        raise SableError(status, where)
+
+
+# ------------------------------------------------------------------ raw calls
+# Same names as the C-ABI; pointers are plain integers (device or host).
+
+def sable_vbr_create(desc: sable_vbr_desc, delta_pct: int, rank: int = 0, world: int = 1,
+                     stream: int = 0) -> int:
+    h = _H()
+    sh = sable_shard(rank, world)
+    _check(_lib.sable_vbr_create(C.byref(desc), delta_pct, C.byref(sh), _P(stream), C.byref(h)),
+           "sable_vbr_create")
+    return h.value
+
+
+def sable_spmv(h: int, x_ptr: int, y_ptr: int, stream: int = 0) -> None:
+    _check(_lib.sable_spmv(_H(h), _P(x_ptr), _P(y_ptr), _P(stream)), "sable_spmv")
+
+
+def sable_spmv_host(h: int, x_ptr: int, y_ptr: int, stream: int = 0) -> None:
+    _check(_lib.sable_spmv_host(_H(h), _P(x_ptr), _P(y_ptr), _P(stream)), "sable_spmv_host")
+
+
+def sable_destroy(h: int) -> None:
+    _check(_lib.sable_destroy(_H(h)), "sable_destroy")
+
+
+def sable_get_info(h: int) -> dict:
+    info = sable_info()
+    _check(_lib.sable_get_info(_H(h), C.byref(info)), "sable_get_info")
+    return {k: getattr(info, k) for k, _ in sable_info._fields_}
+
+
+def sable_export_partition(h: int, out: sable_partition_host) -> None:
+    _check(_lib.sable_export_partition(_H(h), C.byref(out)), "sable_export_partition")
+
+
+def sable_shard_bounds(weights, world: int) -> np.ndarray:
+    w = np.ascontiguousarray(weights, dtype=np.int64)
+    b = np.zeros(world + 1, dtype=np.int32)
+    _check(_lib.sable_shard_bounds(_P(w.ctypes.data), len(w), world, _P(b.ctypes.data)),
+           "sable_shard_bounds")
+    return b
+
+
+def sable_nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(_lib.sable_nccl_unique_id(C.cast(buf, _P)), "sable_nccl_unique_id")
+    return bytes(buf)
+
+
+def sable_comm_init(h: int, uid: bytes) -> None:
+    buf = (C.c_char * 128).from_buffer_copy(uid)
+    _check(_lib.sable_comm_init(_H(h), C.cast(buf, _P)), "sable_comm_init")
+
+
+def sable_spmv_allgather(h: int, x_ptr: int, xn_ptr: int, stream: int = 0) -> None:
+    _check(_lib.sable_spmv_allgather(_H(h), _P(x_ptr), _P(xn_ptr), _P(stream)),
+           "sable_spmv_allgather")
+
+
+def sable_spmv_iterate(h: int, xa_ptr: int, xb_ptr: int, iters: int, stream: int = 0) -> bool:
+    r = C.c_int32(0)
+    _check(_lib.sable_spmv_iterate(_H(h), _P(xa_ptr), _P(xb_ptr), iters, _P(stream), C.byref(r)),
+           "sable_spmv_iterate")
+    return bool(r.value)
+
+
+def sable_status_string(s: int) -> str:
+    return _lib.sable_status_string(s).decode()
+
+
+def sable_last_error() -> str:
+    return _lib.sable_last_error().decode()
+
+
+def sable_abi_version() -> int:
+    return int(_lib.sable_abi_version())
+
+
+# ------------------------------------------------------------ torch front-end
+
+def _dtype_code(dt) -> int:
+    import torch
+    if isinstance(dt, torch.dtype):
+        ok = {torch.float32: SABLE_F32, torch.float64: SABLE_F64}
+    else:
+        dt = np.dtype(dt)
+        ok = {np.dtype(np.float32): SABLE_F32, np.dtype(np.float64): SABLE_F64}
+    if dt not in ok:
+        raise TypeError(f"values must be float32 or float64, got {dt}")
+    return ok[dt]
+
+
+class VbrMatrix:
+    """A handle over libsable.so.  ``arrays`` is a dict with rpntr, cpntr,
+    bpntr, bindx, indx, val and optionally rem_indptr, rem_indices, rem_val
+    (numpy arrays or CUDA torch tensors, all of the same kind)."""
+
+    def __init__(self, arrays: dict, nrows: int, ncols: int, delta: int = 50,
+                 rank: int = 0, world: int = 1, device=None):
+        import torch
+        self.device = torch.device(device or "cuda")
+        keep = []
+        first = arrays["val"]
+        on_dev = isinstance(first, torch.Tensor) and first.is_cuda
+
+        def ptr(name, dt):
+            a = arrays.get(name)
+            if a is None:
+                return None, 0
+            if on_dev:
+                t = a.contiguous()
+                keep.append(t)
+                return t.data_ptr(), t.numel()
+            n = np.ascontiguousarray(a, dtype=dt)
+            keep.append(n)
+            return n.ctypes.data, n.size
+
+        vdt = np.float64 if _dtype_code(first.dtype) == SABLE_F64 else np.float32
+        d = sable_vbr_desc()
+        d.nrows, d.ncols = nrows, ncols
+        d.rpntr, nrp = ptr("rpntr", np.int32)
+        d.cpntr, ncp = ptr("cpntr", np.int32)
+        d.bpntr, _ = ptr("bpntr", np.int64)
+        d.bindx, nblk = ptr("bindx", np.int32)
+        d.indx, _ = ptr("indx", np.int64)
+        d.val, nval = ptr("val", vdt)
+        d.rem_indptr, _ = ptr("rem_indptr", np.int64)
+        d.rem_indices, nrem = ptr("rem_indices", np.int32)
+        d.rem_val, _ = ptr("rem_val", vdt)
+        d.nbrows, d.nbcols = nrp - 1, ncp - 1
+        d.nblocks, d.val_len, d.rem_nnz = nblk, nval, nrem
+        d.dtype = SABLE_F64 if vdt == np.float64 else SABLE_F32
+        d.mem = SABLE_MEM_DEVICE if on_dev else SABLE_MEM_HOST
+        self.dtype = torch.float64 if vdt == np.float64 else torch.float32
+        self.np_dtype = vdt
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream().cuda_stream
+            self.handle = sable_vbr_create(d, int(delta), rank, world, stream)
+        self.info = sable_get_info(self.handle)
+        del keep
+
+    # -- products
+    def spmv(self, x, y=None, stream=None):
+        import torch
+        nloc = self.info["row_end"] - self.info["row_begin"]
+        if y is None:
+            y = torch.empty(nloc, dtype=self.dtype, device=self.device)
+        assert x.dtype == self.dtype and y.dtype == self.dtype and x.is_cuda and y.is_cuda
+        assert x.is_contiguous() and y.is_contiguous() and x.numel() == self.info["ncols"]
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        sable_spmv(self.handle, x.data_ptr(), y.data_ptr(), s)
+        return y
+
+    def spmv_host(self, x: np.ndarray, y: np.ndarray | None = None, stream=None) -> np.ndarray:
+        import torch
+        nloc = self.info["row_end"] - self.info["row_begin"]
+        if y is None:
+            y = np.empty(nloc, dtype=self.np_dtype)
+        assert x.dtype == self.np_dtype and y.dtype == self.np_dtype
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        sable_spmv_host(self.handle, x.ctypes.data, y.ctypes.data, s)
+        return y
+
+    def comm_init(self, uid: bytes):
+        sable_comm_init(self.handle, uid)
+
+    def spmv_allgather(self, x, x_next, stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        sable_spmv_allgather(self.handle, x.data_ptr(), x_next.data_ptr(), s)
+        return x_next
+
+    def iterate(self, x_a, x_b, iters: int, stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        in_b = sable_spmv_iterate(self.handle, x_a.data_ptr(), x_b.data_ptr(), iters, s)
+        return x_b if in_b else x_a
+
+    # -- parity export
+    def export(self) -> dict:
+        i = self.info
+        nc, nd, te, rn = i["n_cells"], i["n_dense"], i["tile_elems"], i["rem_nnz"]
+        nloc = i["row_end"] - i["row_begin"]
+        out = dict(cell_br=np.zeros(nc, np.int32), cell_bc=np.zeros(nc, np.int32),
+                   cell_cnt=np.zeros(nc, np.int64), cell_dense=np.zeros(nc, np.uint8),
+                   tile_off=np.zeros(nd + 1, np.int64), tile_val=np.zeros(te, self.np_dtype),
+                   ublocks=np.zeros(nc - nd, np.int64), rem_indptr=np.zeros(nloc + 1, np.int64),
+                   rem_indices=np.zeros(rn, np.int32), rem_val=np.zeros(rn, self.np_dtype))
+        p = sable_partition_host(**{k: v.ctypes.data for k, v in out.items()})
+        sable_export_partition(self.handle, p)
+        return out
+
+    def close(self):
+        if getattr(self, "handle", None):
+            sable_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
