@@ -1,0 +1,121 @@
+#!/usr/bin/env python
+"""Summarise ncu captures for profiles/ (run here, no GPU needed).
+
+usage: python scripts/ncu_summary.py <dir with spmv_<cfg>.ncu-rep / launches_<cfg>.csv> <out.md>
+
+For every config found: the top metrics of the --set full capture of the
+SpMV kernel (duration, DRAM bytes -> traffic per launch, DRAM / L2 / SM
+throughput %, occupancy, stall reasons) and, from the --metrics
+gpu__time_duration.sum launch list, the SpMV kernel's share of the device
+time of one timed bench step (cold-cache, serialised: compare shares).
+"""
+import csv
+import glob
+import io
+import json
+import os
+import re
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sector_hit_rate.pct",
+    "l1tex__t_sector_hit_rate.pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+    "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
+    "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+]
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6,
+        "usecond": 1e-6, "nsecond": 1e-9, "ms": 1e-3, "msecond": 1e-3}
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    res = []
+    for v in rows[2:]:
+        d = {}
+        for i, k in enumerate(h):
+            d[k] = (v[i], units[i])
+        res.append(d)
+    return res
+
+
+def num(d, k):
+    v, u = d.get(k, ("", ""))
+    try:
+        x = float(v.replace(",", ""))
+    except ValueError:
+        return None
+    return x * UNIT.get(u, 1.0)
+
+
+def launch_shares(path):
+    rows = []
+    with open(path) as f:
+        lines = [ln for ln in f if ln.startswith('"')]
+    for r in csv.DictReader(io.StringIO("".join(lines))):
+        if r.get("Metric Name") == "gpu__time_duration.sum":
+            rows.append((r["Kernel Name"], float(r["Metric Value"].replace(",", "")) *
+                         UNIT.get(r["Metric Unit"], 1.0)))
+    return rows
+
+
+def main():
+    d, out = sys.argv[1], sys.argv[2]
+    lines = [f"# ncu summary: {d}", ""]
+    traffic = {}
+    for rep in sorted(glob.glob(os.path.join(d, "spmv_*.ncu-rep"))):
+        cfg = re.sub(r"^spmv_|\.ncu-rep$", "", os.path.basename(rep))
+        lines.append(f"## {cfg}: `ncu --set full` of the SpMV kernel")
+        for i, k in enumerate(raw(rep)):
+            name = k.get("Kernel Name", ("?", ""))[0]
+            lines.append(f"### launch {i}: {name}")
+            for key in KEYS:
+                if key in k:
+                    lines.append(f"- {key}: {k[key][0]} {k[key][1]}")
+            rd, wr = num(k, "dram__bytes_read.sum"), num(k, "dram__bytes_write.sum")
+            if rd is not None and wr is not None:
+                traffic.setdefault(cfg, int(rd + wr))
+                lines.append(f"- traffic (read+write): {int(rd + wr)} B")
+            stalls = sorted(((float(v[0]), kk) for kk, v in k.items()
+                             if kk.startswith("smsp__pcsamp_warps_issue_stalled_")
+                             and not kk.endswith("_not_issued") and v[0] not in ("",)),
+                            reverse=True)[:6]
+            if stalls:
+                lines.append("- top stall samples: " + ", ".join(
+                    f"{kk.replace('smsp__pcsamp_warps_issue_stalled_', '')}={int(v)}"
+                    for v, kk in stalls))
+        lines.append("")
+    for lf in sorted(glob.glob(os.path.join(d, "launches_*.csv"))):
+        cfg = re.sub(r"^launches_|\.csv$", "", os.path.basename(lf))
+        rows = launch_shares(lf)
+        sp = [t for n, t in rows if "spmv" in n]
+        lines.append(f"## {cfg}: launch list ({len(rows)} launches)")
+        if sp:
+            # the last launches of the run are the timed/kernel-only steps:
+            # one step = one spmv launch (+ the L2 scrub, which is not ours)
+            lines.append(f"- spmv launches: {len(sp)}; median {sorted(sp)[len(sp) // 2] * 1e6:.2f} us")
+        tot = {}
+        for n, t in rows:
+            short = n.split("(")[0]
+            tot[short] = tot.get(short, 0.0) + t
+        for n, t in sorted(tot.items(), key=lambda kv: -kv[1])[:8]:
+            lines.append(f"- {n}: {t * 1e6:.1f} us total")
+        lines.append("")
+    with open(out, "w") as f:
+        f.write("\n".join(lines) + "\n")
+    tj = os.path.join(os.path.dirname(out), "traffic.json")
+    old = json.load(open(tj)) if os.path.exists(tj) else {}
+    old.update(traffic)
+    json.dump(old, open(tj, "w"), indent=1, sort_keys=True)
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
