@@ -253,7 +253,8 @@ def run_sable(args):
                 "grid": [len(s.rpntr) - 1, len(s.cpntr) - 1],
                 "n_cells": info["n_cells"], "n_dense_tiles": info["n_dense"],
                 "tile_elems": info["tile_elems"], "rem_nnz": info["rem_nnz"],
-                "work_items": info["n_items"],
+                "work_items": info["n_items"], "n_tasks": info["n_tasks"],
+                "exec_grid": info["exec_grid"], "item_bytes": info["item_bytes"],
                 "l2": ("flushed between timed steps (512 MiB write)" if flush_l2 else
                        "not flushed: working set > L2 (iterated SpMV, cache behaviour is real)"),
                 "parallelism": f"row-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),

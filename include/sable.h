@@ -133,6 +133,9 @@ typedef struct {
   int32_t suitable;           /* >= 1 dense tile in the matrix */
   int32_t world, rank;
   double inspect_ms;          /* wall time of sable_vbr_create's inspector    */
+  int64_t n_tasks;            /* executor warp tasks (contiguous item ranges) */
+  int32_t exec_grid;          /* CTAs of one sable_spmv launch                */
+  int32_t item_bytes;         /* cap on the bytes one work item streams       */
 } sable_info;
 
 /* Caller-allocated HOST buffers for sable_export_partition, sized from

@@ -27,13 +27,14 @@ sable_status create_impl(const sable_vbr_desc* d, uint32_t delta, const sable_sh
                          cudaStream_t st, sable_handle** out);
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st);
 sable_status comm_destroy(sable_handle* h);
+int32_t exec_grid(const sable_handle* h);
 
 void free_handle(sable_handle* h) {
   if (!h) return;
-  void* dev[] = {h->tval,     h->tiles,      h->groups,   h->items,          h->rem_ptr,
+  void* dev[] = {h->tval,     h->tiles,      h->xt,       h->items,          h->rem_ptr,
                  h->rem_idx,  h->rem_val,    h->scratch,  h->counters,       h->cell_br,
                  h->cell_bc,  h->cell_cnt,   h->cell_dense, h->tile_canon_off, h->tile_br,
-                 h->br_vbase, h->br_W,       h->x_dev,    h->y_dev};
+                 h->br_vbase, h->br_W,       h->xgi,        h->task,       h->chunks,     h->x_dev,    h->y_dev};
   for (void* p : dev)
     if (p) cudaFree(p);
   free(h->all_bounds_h);
@@ -230,6 +231,9 @@ sable_status sable_get_info(const sable_handle* h, sable_info* info) {
   info->world = h->world;
   info->rank = h->rank;
   info->inspect_ms = h->inspect_ms;
+  info->n_tasks = h->cfg.n_tasks;
+  info->exec_grid = exec_grid(h);
+  info->item_bytes = h->cfg.item_bytes;
   return SABLE_OK;
 }
 

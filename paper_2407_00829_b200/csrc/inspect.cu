@@ -306,7 +306,7 @@ __global__ void k_tile_meta(const int32_t* tile_cell, int64_t nt, const int32_t*
 __global__ void k_tile_desc(const int32_t* tile_cell, int64_t nt, const int32_t* cell_bc,
                             const int32_t* tile_br, const int32_t* tile_w,
                             const int64_t* w_scan, const int64_t* br_wprefix, int32_t br_begin,
-                            const int32_t* cpntr, TileDesc* desc) {
+                            const int32_t* cpntr, TileDesc* desc, XTile* xt) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nt) return;
   TileDesc d;
@@ -314,6 +314,8 @@ __global__ void k_tile_desc(const int32_t* tile_cell, int64_t nt, const int32_t*
   d.w = tile_w[t];
   d.cs = (int32_t)(w_scan[t] - br_wprefix[tile_br[t] - br_begin]);
   desc[t] = d;
+  xt[t] = XTile{(int32_t)w_scan[t], d.c0};
+  if (t == nt - 1) xt[nt] = XTile{(int32_t)(w_scan[t] + d.w), 0};  // sentinel
 }
 
 template <typename T>
@@ -442,7 +444,10 @@ void d2h(T* dst, const T* src, int64_t n, cudaStream_t st) {
 template <typename T>
 T* dev_alloc(int64_t n, cudaStream_t st) {
   void* p = nullptr;
-  SB_CU(cudaMallocAsync(&p, sizeof(T) * (size_t)std::max<int64_t>(n, 1), st));
+  // +16 B tail: the executor's 16-byte-rounded bulk copies may read up to
+  // 15 bytes past the last element of an array (never used)
+  SB_CU(cudaMallocAsync(&p, sizeof(T) * (size_t)std::max<int64_t>(n, 1) + 16, st));
+  SB_CU(cudaMemsetAsync(static_cast<char*>(p) + sizeof(T) * (size_t)std::max<int64_t>(n, 1), 0, 16, st));
   return static_cast<T*>(p);
 }
 
@@ -508,6 +513,314 @@ int bits_for(uint64_t v) {  // bits to represent 0..v
 int64_t env_int(const char* name, int64_t dflt) {
   const char* s = std::getenv(name);
   return s ? std::atoll(s) : dflt;
+}
+
+// ------------------------------------------------------------------- a5: plan
+
+// Executor shape; SABLE_* environment variables override the defaults
+// (tuning and tests).  Invalid overrides -> SABLE_E_INVALID_ARG.
+ExecCfg exec_config(int sv) {
+  ExecCfg c;
+  c.stage_bytes = (int32_t)env_int("SABLE_STAGE_BYTES", 3072);
+  c.nstage = (int32_t)env_int("SABLE_NSTAGE", 3);
+  c.item_bytes = (int32_t)env_int("SABLE_ITEM_BYTES", c.stage_bytes - 512);
+  c.xbuf = (int32_t)env_int("SABLE_XBUF", 384);
+  const int64_t per_cta = (int64_t)kWarps * warp_smem_bytes(c.nstage, c.stage_bytes, c.xbuf, sv);
+  c.ctas_per_sm = (int32_t)env_int(
+      "SABLE_CTAS_PER_SM", std::max<int64_t>(1, std::min<int64_t>(8, (227 * 1024) / per_cta)));
+  c.mode = (int32_t)env_int("SABLE_EXEC_MODE", 0);
+  c.n_tasks = (int32_t)env_int("SABLE_TASKS", 0);  // 0 = one per executor warp
+  const bool ok = c.stage_bytes % 128 == 0 && c.stage_bytes <= 65536 && c.nstage >= 2 &&
+                  c.nstage <= kMaxStages && c.item_bytes >= 4 * sv &&
+                  c.item_bytes + 256 <= c.stage_bytes && c.xbuf >= 64 && c.xbuf <= 16384 &&
+                  c.ctas_per_sm >= 1 &&
+                  per_cta * c.ctas_per_sm <= 227 * 1024 && c.n_tasks >= 0;
+  if (!ok) {
+    set_error("invalid SABLE_STAGE_BYTES / SABLE_NSTAGE / SABLE_ITEM_BYTES / SABLE_XBUF / "
+              "SABLE_CTAS_PER_SM / SABLE_TASKS combination");
+    throw Fail{SABLE_E_INVALID_ARG};
+  }
+  return c;
+}
+
+int device_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+// Work items (row groups or pieces of them) and warp tasks (contiguous item
+// ranges of about equal bytes, one per executor warp).  Items depend only on
+// the block rows, and a group's pieces are summed left to right whoever
+// processes them, so y is identical for every shard count.
+template <typename T>
+void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
+                   const std::vector<int32_t>& H_rpntr, const std::vector<int32_t>& H_W,
+                   const std::vector<int64_t>& br_vbase, const std::vector<int64_t>& br_wprefix,
+                   const std::vector<int32_t>& H_rp, const std::vector<XTile>& H_tile,
+                   cudaStream_t st) {
+  const int64_t sv = sizeof(T);
+  const int64_t cap = cfg.item_bytes;
+
+  // runs: adjacent tiles whose flattened and global columns advance together
+  std::vector<XTile> R;
+  const int64_t ntile = (int64_t)H_tile.size() - 1;
+  for (int64_t t = 0; t < ntile; ++t) {
+    if (!R.empty() && (int64_t)H_tile[t].c0 - H_tile[t].tp == (int64_t)R.back().c0 - R.back().tp)
+      continue;
+    R.push_back(H_tile[t]);
+  }
+  const int64_t nrun = (int64_t)R.size();
+  R.push_back(XTile{ntile > 0 ? H_tile[ntile].tp : 0, 0});  // sentinel
+  auto run_of = [&](int64_t pc) {  // last run with tp <= pc
+    return (int64_t)(std::upper_bound(R.begin(), R.begin() + nrun, pc,
+                                      [](int64_t v, const XTile& t) { return v < (int64_t)t.tp; }) -
+                     R.begin() - 1);
+  };
+
+  std::vector<Item> It;
+  std::vector<XgInfo> Xg;
+  std::vector<int64_t> Ib;  // streamed bytes per item
+  It.reserve((size_t)(H_rp.size() / 8 + nbl + 1));
+  int64_t slot = 0, ngroups = 0;
+  for (int32_t la = 0; la < nbl; ++la) {
+    const int32_t a = b0 + la;
+    const int32_t hgt = H_rpntr[a + 1] - H_rpntr[a];
+    const int64_t W = H_W[a];
+    const int32_t r0 = (int32_t)(H_rpntr[a] - h->row_begin);
+    const int64_t xp = br_wprefix[la];
+    for (int32_t j = 0; j * kGroupRows < hgt; ++j) {
+      Item base{};
+      base.row0 = r0 + j * kGroupRows;
+      const int nr = std::min(kGroupRows, hgt - j * kGroupRows);
+      base.nr = (uint8_t)nr;
+      base.q = (uint8_t)(32 / nr);
+      base.qm = (uint16_t)(32768 / nr + 1);
+      const int64_t voff = br_vbase[la] + (int64_t)j * kGroupRows * W;
+      const int64_t eb = H_rp[base.row0], ee = H_rp[base.row0 + nr];
+      const int64_t dbytes = W * nr * sv, rbytes = (ee - eb) * (sv + 4);
+      const size_t first = It.size();
+      const int64_t k0 = W > 0 ? run_of(xp) : 0;
+      const bool one_run = W == 0 || (int64_t)R[k0 + 1].tp >= xp + W;
+      if (one_run && dbytes + rbytes + 32 <= cap && ee - eb <= kRE && W + (ee - eb) <= cfg.xbuf) {
+        Item it = base;
+        it.voff = voff;
+        it.eb = (int32_t)eb;
+        it.ne = (int16_t)(ee - eb);
+        it.ncol = (int16_t)W;
+        it.xo = W > 0 ? (int32_t)(R[k0].c0 - R[k0].tp + xp) : 0;
+        It.push_back(it);
+        Ib.push_back(dbytes + rbytes + 32);
+      } else {
+        // dense pieces: column ranges inside one run, <= cap bytes each
+        const int64_t dc = std::max<int64_t>(
+            1, std::min<int64_t>(cfg.xbuf, (cap - 32) / (nr * sv)));
+        int64_t c = 0, k = k0;
+        while (c < W) {
+          const int64_t run_end = std::min<int64_t>(W, (int64_t)R[k + 1].tp - xp);
+          const int64_t ce = std::min(run_end, c + dc);
+          Item it = base;
+          it.voff = voff + c * nr;
+          it.eb = (int32_t)ee;
+          it.ncol = (int16_t)(ce - c);
+          it.xo = (int32_t)(R[k].c0 - R[k].tp + xp + c);
+          It.push_back(it);
+          Ib.push_back((ce - c) * nr * sv + 32);
+          c = ce;
+          if (c >= run_end) ++k;
+        }
+        const int64_t rc = std::max<int64_t>(
+            1, std::min<int64_t>(std::min<int64_t>(kRE, cfg.xbuf), (cap - 32) / (sv + 4)));
+        for (int64_t e = eb; e < ee; e += rc) {
+          Item it = base;
+          it.voff = voff;
+          it.eb = (int32_t)e;
+          it.ne = (int16_t)(std::min(ee, e + rc) - e);
+          It.push_back(it);
+          Ib.push_back(it.ne * (sv + 4) + 32);
+        }
+        if (It.size() == first) {
+          It.push_back(base);
+          Ib.push_back(32);
+        }
+      }
+      const int64_t np = (int64_t)(It.size() - first);
+      for (size_t q = first; q < It.size(); ++q) {
+        It[q].flags = (uint8_t)((q == first ? IF_FIRST : 0) | (q + 1 == It.size() ? IF_LAST : 0));
+        XgInfo xi{};
+        xi.slot = np > 1 ? slot : 0;
+        xi.g = (int32_t)ngroups;
+        xi.p = (int16_t)std::min<int64_t>(q - first, 32767);
+        xi.npieces = (int32_t)np;
+        Xg.push_back(xi);
+      }
+      if (np > 32767) {
+        set_error("a row group needs more than 32767 work items");
+        throw Fail{SABLE_E_UNSUPPORTED};
+      }
+      if (np > 1) slot += np * kGroupRows;
+      ++ngroups;
+    }
+  }
+  const int64_t nit = (int64_t)It.size();
+
+  // chunks: greedy runs of consecutive items whose five ranges (items, row
+  // pointers, values, remainder columns, remainder values; each rounded out
+  // to 16 bytes) fit one stage after the 64-byte descriptor slot
+  struct Acc {
+    int64_t i0 = 0, ni = 0, vlo = 0, vhi = 0, elo = 0, ehi = 0, rlo = 0, rhi = 0, ndx = 0;
+    bool dv = false, de = false;
+  };
+  auto extend = [&](Acc A, int64_t i) {
+    const Item& it = It[i];
+    if (A.ni == 0) A.i0 = i;
+    A.ni++;
+    A.ndx += it.ncol;
+    if (it.ncol > 0) {
+      const int64_t v0 = it.voff, v1 = it.voff + (int64_t)it.ncol * it.nr;
+      if (!A.dv) { A.vlo = v0; A.vhi = v1; A.dv = true; }
+      else { A.vlo = std::min(A.vlo, v0); A.vhi = std::max(A.vhi, v1); }
+    }
+    if (it.ne > 0) {
+      const int64_t e0 = it.eb, e1 = (int64_t)it.eb + it.ne;
+      if (!A.de) { A.elo = e0; A.ehi = e1; A.rlo = it.row0; A.rhi = it.row0 + it.nr; A.de = true; }
+      else {
+        A.elo = std::min(A.elo, e0); A.ehi = std::max(A.ehi, e1);
+        A.rlo = std::min<int64_t>(A.rlo, it.row0); A.rhi = std::max<int64_t>(A.rhi, it.row0 + it.nr);
+      }
+    }
+    return A;
+  };
+  struct Rng { int64_t first, count; int es; };
+  auto ranges = [&](const Acc& A, Rng* r) {
+    r[SR_ITEM] = {A.i0, A.ni, (int)sizeof(Item)};
+    r[SR_RPTR] = {A.rlo, A.de ? A.rhi - A.rlo + 1 : 0, 4};
+    r[SR_VAL] = {A.vlo, A.dv ? A.vhi - A.vlo : 0, (int)sv};
+    r[SR_RIDX] = {A.elo, A.de ? A.ehi - A.elo : 0, 4};
+    r[SR_RVAL] = {A.elo, A.de ? A.ehi - A.elo : 0, (int)sv};
+  };
+  auto bytes_of = [&](const Acc& A) {
+    if (A.ndx + (A.de ? A.ehi - A.elo : 0) > cfg.xbuf || A.ni > 32767)
+      return (int64_t)cfg.stage_bytes + 1;  // the chunk's x would not fit the buffer
+    Rng r[SR_N];
+    ranges(A, r);
+    int64_t o = 64;
+    for (int k = 0; k < SR_N; ++k) {
+      if (r[k].count <= 0) continue;
+      const int64_t a0 = r[k].first * r[k].es, a1 = a0 + r[k].count * r[k].es;
+      o += ((a1 + 15) & ~(int64_t)15) - (a0 & ~(int64_t)15);
+    }
+    return o;
+  };
+  std::vector<Chunk> Ch;
+  std::vector<int64_t> Cb;
+  auto push = [&](const Acc& A) {
+    Rng r[SR_N];
+    ranges(A, r);
+    Chunk c{};
+    int64_t o = 64;
+    for (int k = 0; k < SR_N; ++k) {
+      if (r[k].count <= 0) continue;
+      const int64_t a0 = r[k].first * r[k].es, a1 = a0 + r[k].count * r[k].es;
+      const int64_t A0 = a0 & ~(int64_t)15, A1 = (a1 + 15) & ~(int64_t)15;
+      c.src16[k] = (uint32_t)(A0 / 16);
+      c.bytes[k] = (uint16_t)(A1 - A0);
+      c.off[k] = (uint16_t)(o + (a0 - A0));
+      o += A1 - A0;
+    }
+    c.v0 = A.vlo;
+    c.e0 = (int32_t)A.elo;
+    c.r0 = (int32_t)A.rlo;
+    c.ni = (int16_t)A.ni;
+    c.ndx = (int16_t)A.ndx;
+    c.i0 = (int32_t)A.i0;
+    int64_t xb = 0;
+    for (int64_t q = A.i0; q < A.i0 + A.ni; ++q) {
+      It[q].xb = (int16_t)xb;
+      xb += It[q].ncol;
+    }
+    Ch.push_back(c);
+    Cb.push_back(o);
+  };
+  {
+    Acc cur;
+    for (int64_t i = 0; i < nit; ++i) {
+      Acc nxt = extend(cur, i);
+      if (cur.ni > 0 && bytes_of(nxt) > cfg.stage_bytes) {
+        push(cur);
+        nxt = extend(Acc{}, i);
+      }
+      if (bytes_of(nxt) > cfg.stage_bytes) {
+        set_error("internal: a work item does not fit one executor stage");
+        throw Fail{SABLE_E_UNSUPPORTED};
+      }
+      cur = nxt;
+    }
+    if (cur.ni > 0) push(cur);
+  }
+  const int64_t nch = (int64_t)Ch.size();
+  if (nch > 0 && (int64_t)(It.size() * sizeof(Item)) / 16 > (int64_t)UINT32_MAX) {
+    set_error("executor arrays exceed the 64 GiB bulk-copy offset range");
+    throw Fail{SABLE_E_UNSUPPORTED};
+  }
+
+  // warp tasks: contiguous chunk ranges of about equal bytes; a cut moves to
+  // the next group boundary when one is near, so only groups larger than a
+  // fraction of a task are shared between warps (and combined in scratch)
+  const int64_t grid = (int64_t)device_sms() * cfg.ctas_per_sm;
+  const int64_t ntask = cfg.n_tasks > 0 ? cfg.n_tasks : std::max<int64_t>(1, grid * kWarps);
+  cfg.n_tasks = (int32_t)ntask;
+  std::vector<int64_t> cpre(nch + 1, 0);
+  for (int64_t k = 0; k < nch; ++k) cpre[k + 1] = cpre[k] + Cb[k];
+  std::vector<int32_t> task(ntask + 1, 0);
+  auto starts_group = [&](int64_t k) { return (It[Ch[k].i0].flags & IF_FIRST) != 0; };
+  {
+    int64_t k = 0;
+    const int64_t slack = std::max<int64_t>(1, (cpre[nch] / ntask) / 4);
+    for (int64_t t = 1; t < ntask; ++t) {
+      const int64_t target = cpre[nch] * t / ntask;
+      while (k < nch && cpre[k] < target) ++k;
+      int64_t kk = k;  // boundary before chunk kk: prefer one that starts a group
+      while (kk < nch && !starts_group(kk) && cpre[kk] - target < slack) ++kk;
+      if (kk < nch && !starts_group(kk)) kk = k;
+      k = std::max<int64_t>(kk, task[t - 1]);
+      task[t] = (int32_t)k;
+    }
+    task[ntask] = (int32_t)nch;
+  }
+  // groups with pieces in more than one task combine through global scratch
+  for (int64_t t = 1; t < ntask; ++t) {
+    const int64_t k = task[t];
+    if (k <= 0 || k >= nch) continue;
+    const int64_t i = Ch[k].i0;
+    if (It[i].flags & IF_FIRST) continue;
+    int64_t g0 = i;
+    while (!(It[g0].flags & IF_FIRST)) --g0;
+    for (int64_t q = g0; q < g0 + Xg[g0].npieces; ++q) It[q].flags |= IF_XG;
+  }
+
+  h->n_groups = ngroups;
+  h->n_items = nit;
+  h->n_chunks = nch;
+  h->n_runs = nrun;
+  h->chunks = dev_alloc<Chunk>(nch, st);
+  if (nch) SB_CU(cudaMemcpyAsync(h->chunks, Ch.data(), sizeof(Chunk) * nch, cudaMemcpyHostToDevice, st));
+  h->items = dev_alloc<Item>(nit, st);
+  h->xgi = dev_alloc<XgInfo>(nit, st);
+  h->task = dev_alloc<int32_t>(ntask + 1, st);
+  if (nit) {
+    SB_CU(cudaMemcpyAsync(h->items, It.data(), sizeof(Item) * nit, cudaMemcpyHostToDevice, st));
+    SB_CU(cudaMemcpyAsync(h->xgi, Xg.data(), sizeof(XgInfo) * nit, cudaMemcpyHostToDevice, st));
+  }
+  SB_CU(cudaMemcpyAsync(h->task, task.data(), sizeof(int32_t) * (ntask + 1), cudaMemcpyHostToDevice, st));
+  h->scratch_elems = slot;
+  h->scratch = dev_alloc<T>(slot, st);
+  h->counters = dev_alloc<int32_t>(ngroups, st);
+  SB_CU(cudaMemsetAsync(h->counters, 0, sizeof(int32_t) * std::max<int64_t>(ngroups, 1), st));
+  SB_CU(cudaStreamSynchronize(st));  // It / Xg / R / Ch / task are host temporaries
+  cudaFree(h->xt);  // the per-tile map was only needed to plan
+  h->xt = nullptr;
 }
 
 // ------------------------------------------------------------------- inspect
@@ -708,6 +1021,11 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
   }
   br_vbase[nbl] = tile_elems;
   br_t0[nbl] = n_dense;
+  br_wprefix[nbl] = nbl ? br_wprefix[nbl - 1] + H_W[b1 - 1] : 0;
+  if (br_wprefix[nbl] > INT32_MAX - 1) {
+    set_error("local dense tiles span more than 2^31-1 panel columns");
+    throw Fail{SABLE_E_UNSUPPORTED};
+  }
   const int64_t cell_hi = cell_lo + n_cells;
   h->cell_base = cell_lo;
   h->n_cells = n_cells;
@@ -745,6 +1063,8 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
   }
   h->tile_br = dev_alloc<int32_t>(n_dense, st);
   h->tiles = dev_alloc<TileDesc>(n_dense, st);
+  h->xt = dev_alloc<XTile>(n_dense + 1, st);
+  SB_CU(cudaMemsetAsync(h->xt, 0, sizeof(XTile) * (n_dense + 1), st));
   h->tile_canon_off = dev_alloc<int64_t>(n_dense + 1, st);
   h->br_vbase = dev_alloc<int64_t>(nbl + 1, st);
   h->br_W = dev_alloc<int32_t>(nbl + 1, st);
@@ -772,7 +1092,7 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
     cub_run([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, tw64, ws, n_dense, st); }, st);
     k_tile_desc<<<nblocks_for(n_dense, TH), TH, 0, st>>>(tile_cell, n_dense, cell_bc, h->tile_br,
                                                          tw, ws, wpre_b.as<int64_t>(), b0,
-                                                         in.cpntr, h->tiles);
+                                                         in.cpntr, h->tiles, h->xt);
   }
   h->tval = dev_alloc<T>(tile_elems, st);
   SB_CU(cudaMemsetAsync(h->tval, 0, sizeof(T) * std::max<int64_t>(tile_elems, 1), st));
@@ -900,61 +1220,12 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
   // ---- a5: plan (host) ---------------------------------------------------------------
   std::vector<int32_t> H_rp(nloc + 1);
   d2h(H_rp.data(), h->rem_ptr, nloc + 1, st);
+  std::vector<XTile> H_xt(n_dense + 1);
+  d2h(H_xt.data(), h->xt, n_dense + 1, st);
   SB_CU(cudaStreamSynchronize(st));
-  const int64_t cap = env_int("SABLE_PIECE_BYTES", 8192);
-  std::vector<Group> G;
-  std::vector<Item> It;
-  int64_t slot = 0;
-  G.reserve(nloc / 8 + nbl + 1);
-  for (int32_t la = 0; la < nbl; ++la) {
-    const int32_t a = b0 + la;
-    const int32_t hgt = H_rpntr[a + 1] - H_rpntr[a];
-    const int32_t W = H_W[a];
-    const int32_t r0 = (int32_t)(H_rpntr[a] - h->row_begin);
-    for (int32_t j = 0; j * kGroupRows < hgt; ++j) {
-      Group g{};
-      g.row0 = r0 + j * kGroupRows;
-      g.nr = std::min(kGroupRows, hgt - j * kGroupRows);
-      g.t0 = (int32_t)br_t0[la];
-      g.t1 = (int32_t)br_t0[la + 1];
-      g.W = W;
-      g.voff = br_vbase[la] + (int64_t)j * kGroupRows * W;
-      const int64_t eb = H_rp[g.row0], ee = H_rp[g.row0 + g.nr];
-      const int64_t dbytes = (int64_t)g.nr * W * (int64_t)sv;
-      const int64_t rbytes = (ee - eb) * (int64_t)(sv + 4);
-      const int32_t gi = (int32_t)G.size();
-      int32_t np = 0;
-      if (dbytes + rbytes <= cap && W <= kXCap) {
-        It.push_back(Item{eb, ee, gi, 0, 0, W});
-        np = 1;
-      } else {
-        const int64_t dc = std::max<int64_t>(1, std::min<int64_t>(kXCap, cap / ((int64_t)g.nr * (int64_t)sv)));
-        for (int64_t cb = 0; cb < W; cb += dc)
-          It.push_back(Item{0, 0, gi, np++, (int32_t)cb, (int32_t)std::min<int64_t>(W, cb + dc)});
-        const int64_t rc = std::max<int64_t>(kWin, cap / (int64_t)(sv + 4));
-        for (int64_t e = eb; e < ee; e += rc)
-          It.push_back(Item{e, std::min(ee, e + rc), gi, np++, 0, 0});
-        if (np == 0) It.push_back(Item{0, 0, gi, np++, 0, 0});
-      }
-      g.npieces = np;
-      g.slot = 0;
-      if (np > 1) {
-        g.slot = slot;
-        slot += (int64_t)np * kGroupRows;
-      }
-      G.push_back(g);
-    }
-  }
-  h->n_groups = (int64_t)G.size();
-  h->n_items = (int64_t)It.size();
-  h->groups = dev_alloc<Group>(h->n_groups, st);
-  h->items = dev_alloc<Item>(h->n_items, st);
-  if (h->n_groups) SB_CU(cudaMemcpyAsync(h->groups, G.data(), sizeof(Group) * G.size(), cudaMemcpyHostToDevice, st));
-  if (h->n_items) SB_CU(cudaMemcpyAsync(h->items, It.data(), sizeof(Item) * It.size(), cudaMemcpyHostToDevice, st));
-  h->scratch_elems = slot;
-  h->scratch = dev_alloc<T>(slot, st);
-  h->counters = dev_alloc<int32_t>(h->n_groups, st);
-  SB_CU(cudaMemsetAsync(h->counters, 0, sizeof(int32_t) * std::max<int64_t>(h->n_groups, 1), st));
+  ExecCfg cfg = exec_config((int)sv);
+  plan_executor<T>(h, cfg, nbl, b0, H_rpntr, H_W, br_vbase, br_wprefix, H_rp, H_xt, st);
+  h->cfg = cfg;
 
   // ---- bookkeeping ---------------------------------------------------------------------
   int64_t nnz = 0;
@@ -965,10 +1236,11 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
     for (int64_t c : cc) nnz += c;
   }
   h->nnz = nnz;
-  // algorithmic bytes per SpMV: tile values + tile descriptors +
-  // group/item descriptors + remainder (value, index) + row pointers + x + y
-  h->bytes_alg = tile_elems * (int64_t)sv + n_dense * (int64_t)sizeof(TileDesc) +
-                 h->n_groups * (int64_t)sizeof(Group) + h->n_items * (int64_t)sizeof(Item) +
+  // algorithmic bytes per SpMV: tile values + item and
+  // chunk descriptors + remainder (value, index) + row
+  // pointers + x read once + y written once
+  h->bytes_alg = tile_elems * (int64_t)sv + h->n_items * (int64_t)sizeof(Item) +
+                 h->n_chunks * (int64_t)sizeof(Chunk) +
                  n_rem * (int64_t)(sv + 4) + (nloc + 1) * 4 + ncols * (int64_t)sv +
                  nloc * (int64_t)sv;
   SB_CU(cudaStreamSynchronize(st));

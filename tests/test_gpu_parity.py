@@ -147,18 +147,24 @@ def test_shapes(sable, shape, dt):
     A.close()
 
 
-def test_long_remainder_rows(sable):
-    """Rows with thousands of remainder entries are split over several work
-    items and combined in a fixed order (bitwise equal to the oracle on small
-    integers)."""
+def long_rows_synth():
     g = np.random.default_rng(3)
     A_ = np.zeros((40, 20000))
     A_[5, :] = g.integers(1, 4, 20000)            # a full row (remainder at delta = 101)
     A_[7, g.choice(20000, 9000, replace=False)] = 2.0
     A_[20:23, :] = (g.random((3, 20000)) < 0.1) * 3.0
+    A_[30:40, :50] = g.integers(1, 3, (10, 50))   # medium rows: warp-cooperative sums
     rp = [0, 5, 6, 7, 8, 40]
     cp = [0, 5000, 10000, 15000, 20000]
-    s = from_dense(A_, rp, cp, np.float32, 101, g.integers(-2, 3, 20000).astype(np.float32))
+    return from_dense(A_, rp, cp, np.float32, 101, g.integers(-2, 3, 20000).astype(np.float32),
+                      name="longrows")
+
+
+def test_long_remainder_rows(sable):
+    """Rows with thousands of remainder entries are split over several work
+    items and combined in a fixed order (bitwise equal to the oracle on small
+    integers)."""
+    s = long_rows_synth()
     M, _ = check(sable, s, "all_rem", exact=True)
     assert M.info["n_items"] > M.info["n_groups"]
     M.close()
@@ -361,3 +367,46 @@ def test_full_size_sampled(sable, name):
     yo, so = oracle.spmv_rows(s.rowptr(), s.J, s.V.astype(np.float64), s.x.astype(np.float64), rows)
     assert_y_close(y[rows], yo, so, s.dtype, name)
     A.close()
+
+
+# ------------------------------------------------------------------ executor shapes
+
+EXEC_CFGS = {
+    # tiny stages and items: every group split into one-column / few-entry
+    # pieces, many chunks per warp (the stage ring wraps), and an odd task
+    # count that cuts inside groups (pieces meet in global scratch)
+    "tiny": dict(SABLE_STAGE_BYTES=1024, SABLE_ITEM_BYTES=64, SABLE_NSTAGE=2, SABLE_XBUF=64,
+                 SABLE_TASKS=997),
+    # a single warp walks every chunk (deep ring, running sums)
+    "onewarp": dict(SABLE_STAGE_BYTES=2048, SABLE_NSTAGE=4, SABLE_TASKS=1),
+    "wide": dict(SABLE_STAGE_BYTES=8192, SABLE_ITEM_BYTES=4096, SABLE_NSTAGE=2, SABLE_XBUF=1024,
+                 SABLE_TASKS=3),
+}
+
+
+@pytest.mark.parametrize("cfg", sorted(EXEC_CFGS))
+def test_executor_configurations(sable, monkeypatch, cfg):
+    """The same parity bar under other executor shapes (SABLE_* overrides):
+    chunk boundaries, split groups and the stage ring at every position."""
+    for k, v in EXEC_CFGS[cfg].items():
+        monkeypatch.setenv(k, str(v))
+    cases = [gen.make("c1"), gen.make("c2", scale=0.02)]
+    for seed, shape in enumerate([(1000, 800, 7, 5), (64, 5000, 2, 3), (300, 300, 300, 300),
+                                  (517, 611, 40, 3)]):
+        cases.append(gen.random_small(20 + seed, *shape, dtype=np.float64 if seed % 2 else np.float32,
+                                      density=0.2, dense_cells=0.5,
+                                      values="int" if seed == 3 else "u11"))
+    cases.append(long_rows_synth())
+    for s in cases:
+        for split in ("rect", "all_rem"):
+            A, _ = check(sable, s, split, exact=s.name in ("rand23", "longrows"))
+            assert A.info["n_tasks"] == EXEC_CFGS[cfg]["SABLE_TASKS"]
+            A.close()
+
+
+def test_executor_config_rejected(sable, monkeypatch):
+    monkeypatch.setenv("SABLE_ITEM_BYTES", "8")  # smaller than one value per row
+    s = gen.make("c1")
+    with pytest.raises(sable.SableError) as e:
+        handle(sable, s, "rect")
+    assert e.value.status == sable.SABLE_E_INVALID_ARG
