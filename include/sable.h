@@ -136,6 +136,8 @@ typedef struct {
   int64_t n_tasks;            /* executor warp tasks (contiguous item ranges) */
   int32_t exec_grid;          /* CTAs of one sable_spmv launch                */
   int32_t item_bytes;         /* cap on the bytes one work item streams       */
+  int64_t rem_packets;        /* remainder executor warps (row packets)       */
+  int64_t rem_long_pieces;    /* pieces of remainder rows cut across warps    */
 } sable_info;
 
 /* Caller-allocated HOST buffers for sable_export_partition, sized from

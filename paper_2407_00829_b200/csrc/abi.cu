@@ -31,11 +31,14 @@ int32_t exec_grid(const sable_handle* h);
 
 void free_handle(sable_handle* h) {
   if (!h) return;
-  void* dev[] = {h->tval,     h->tiles,      h->xt,       h->items,          h->rem_ptr,
+  void* dev[] = {h->tval,     h->tiles,      h->xt,       h->rem_ptr,
                  h->rem_idx,  h->rem_val,    h->scratch,  h->counters,       h->cell_br,
                  h->cell_bc,  h->cell_cnt,   h->cell_dense, h->tile_canon_off, h->tile_br,
-                 h->br_vbase, h->br_W,       h->xgi,        h->task,       h->chunks,     h->x_dev,    h->y_dev};
+                 h->br_vbase, h->br_W,       h->xgi,        h->task,       h->cref,       h->stream,     h->x_dev,    h->y_dev};
   for (void* p : dev)
+    if (p) cudaFree(p);
+  void* rdev[] = {h->rp.packets, h->rp.scratch, h->rp.counters};
+  for (void* p : rdev)
     if (p) cudaFree(p);
   free(h->all_bounds_h);
   free(h->rpntr_h);
@@ -234,6 +237,8 @@ sable_status sable_get_info(const sable_handle* h, sable_info* info) {
   info->n_tasks = h->cfg.n_tasks;
   info->exec_grid = exec_grid(h);
   info->item_bytes = h->cfg.item_bytes;
+  info->rem_packets = h->rp.n_packets;
+  info->rem_long_pieces = h->rp.n_pieces;
   return SABLE_OK;
 }
 

@@ -8,27 +8,23 @@
 // blocks, re-designed as one data-driven sm_100a kernel
 // instead of generated per-block C.
 //
-// Every warp owns a task: a contiguous range of chunks of about equal bytes
-// (cut at row-group boundaries).  A chunk is a run of consecutive work items
-// whose data are contiguous ranges of five arrays (item descriptors,
-// remainder row pointers, dense values, remainder columns, remainder
-// values).  Lane 0 streams the warp's chunks through a private ring of
-// shared-memory stages with 1-D bulk copies (cp.async.bulk, L2 evict-first,
-// completion on the stage's mbarrier; ranges precomputed by the planner);
-// each stage also carries the descriptor of the chunk nstage ahead, so no
-// warp waits on a descriptor load and no warp waits on another.  Per item:
-//   (1) dense slab: lane l works on row l % nr and column phase l / nr of the
-//       column-major slab in shared memory; items never span a run of
-//       consecutive global columns, so the x of column c is x[xo + c], read
-//       through L1 (the next item's x lines are prefetched into L1 while
-//       this one computes) and broadcast to the lanes of a phase; rows
-//       accumulate in registers and the phases fold with shuffles;
-//   (2) remainder: lanes multiply the staged entries by gathered x into the
-//       warp's product buffer (the next item's x prefetched likewise); lane
-//       r sums row r (the whole warp for long rows);
-//   (3) y: a row is written once.  Pieces of a split group are summed left to
-//       right in registers; a group shared by two tasks meets in global
-//       scratch, where the last piece to arrive sums all pieces in order.
+// The input is one byte stream of self-describing chunks (built by the
+// inspector).  Every warp owns a task: a contiguous range of chunks of about
+// equal bytes.  Lane 0 streams the task's chunks through a private ring of
+// shared-memory stages, ONE 1-D bulk copy per chunk (cp.async.bulk, L2
+// evict-first, completion on the stage's mbarrier); a chunk's header names
+// the chunk nstage ahead, so no warp ever waits on a descriptor and no warp
+// waits on another.  While chunk k is computed, the x it needs for chunk
+// k + 1 (its dense columns' segments and one x per remainder entry) is
+// copied into the other half of the warp's x buffer with 4/8-byte
+// asynchronous copies (LDGSTS).  Chunk k is computed bundle by bundle: a
+// bundle maps the 32 lanes onto the rows of several items -- lane = (item,
+// row r, phase ph of Q) -- chosen by the planner so that the lanes' work is
+// even; a lane sums columns ph, ph + Q, ... of its row of the column-major
+// slab and entries ph, ph + Q, ... of its row's remainder, all from shared
+// memory; the phases fold with shuffles; the row is written once.  Pieces of
+// a group larger than a stage are summed left to right in registers (or, if
+// two tasks share the group, in global scratch by the last piece to arrive).
 // No atomics on y; every row's summation order depends on the matrix alone,
 // so y is bitwise reproducible and identical for every shard count.
 #include "sable_internal.cuh"
@@ -39,7 +35,6 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = kWarps * 32;
-constexpr int kLongRow = 32;  // remainder rows longer than this: whole warp
 
 // ---------------------------------------------------------------- PTX glue
 
@@ -76,6 +71,23 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// 4- or 8-byte asynchronous global -> shared copy (LDGSTS, through L1).
+template <typename T>
+__device__ __forceinline__ void cp_async(T* dst, const T* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "n"((int)sizeof(T))
+               : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
                                          uint32_t bar, uint64_t policy) {
   asm volatile(
@@ -100,154 +112,114 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-// ---------------------------------------------------------------- staging
+// ---------------------------------------------------------------- chunks
 
-// Lane 0: start the copies of chunk c (and of the descriptor of chunk
-// `ahead`, if >= 0, into the stage's first 64 bytes).
-template <typename T>
-__device__ __forceinline__ void issue_chunk(const Plan<T>& P, const Chunk& c, int64_t ahead,
+// Lane 0: start the copy of a chunk into a stage.
+__device__ __forceinline__ void issue_chunk(const unsigned char* stream, const ChunkRef& c,
                                             unsigned char* stage, uint32_t bar, uint64_t pol) {
-  uint32_t tx = ahead >= 0 ? 64u : 0u;
-#pragma unroll
-  for (int k = 0; k < SR_N; ++k) tx += c.bytes[k];
-  mbar_expect_tx(bar, tx);
-  const uint32_t s0 = smem_u32(stage);
-  if (ahead >= 0) bulk_g2s(s0, P.chunks + ahead, 64u, bar, pol);
-  const unsigned char* base[SR_N] = {
-      reinterpret_cast<const unsigned char*>(P.items),
-      reinterpret_cast<const unsigned char*>(P.rem_ptr),
-      reinterpret_cast<const unsigned char*>(P.tval),
-      reinterpret_cast<const unsigned char*>(P.rem_idx),
-      reinterpret_cast<const unsigned char*>(P.rem_val)};
-#pragma unroll
-  for (int k = 0; k < SR_N; ++k)
-    if (c.bytes[k])
-      bulk_g2s(s0 + (c.off[k] & ~15u), base[k] + (size_t)c.src16[k] * 16, c.bytes[k], bar, pol);
+  mbar_expect_tx(bar, (uint32_t)c.bytes);
+  bulk_g2s(smem_u32(stage), stream + c.off, (uint32_t)c.bytes, bar, pol);
 }
 
-// ---------------------------------------------------------------- items
-
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// 4- or 8-byte asynchronous global -> shared copy (LDGSTS, through L1).
+// Start copying the x a staged chunk needs into an x buffer: the dense
+// segments (contiguous global columns), then one x per remainder entry.
+// Asynchronous (LDGSTS): it overlaps the computation of the previous chunk.
 template <typename T>
-__device__ __forceinline__ void cp_async(T* dst, const T* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "n"((int)sizeof(T))
-               : "memory");
-}
-
-template <typename T>
-struct StageView {
-  const Item* items;
-  const int32_t* rptr;
-  const T* val;
-  const int32_t* ridx;
-  const T* rval;
-  int64_t v0;
-  int32_t e0, r0, ni, ndx;
-};
-
-template <typename T>
-__device__ __forceinline__ StageView<T> stage_view(unsigned char* stage, const Chunk& C) {
-  StageView<T> S;
-  S.items = reinterpret_cast<const Item*>(stage + C.off[SR_ITEM]);
-  S.rptr = reinterpret_cast<const int32_t*>(stage + C.off[SR_RPTR]);
-  S.val = reinterpret_cast<const T*>(stage + C.off[SR_VAL]);
-  S.ridx = reinterpret_cast<const int32_t*>(stage + C.off[SR_RIDX]);
-  S.rval = reinterpret_cast<const T*>(stage + C.off[SR_RVAL]);
-  S.v0 = C.v0;
-  S.e0 = C.e0;
-  S.r0 = C.r0;
-  S.ni = C.ni;
-  S.ndx = C.ndx;
-  return S;
-}
-
-// Start copying the x a staged chunk needs into an x buffer: each item's
-// dense columns (contiguous: items never span a run), then one x per
-// remainder entry.  Asynchronous (LDGSTS): it overlaps the previous chunk.
-template <typename T>
-__device__ __forceinline__ void gather_chunk(const StageView<T>& S, T* xb,
+__device__ __forceinline__ void gather_chunk(const unsigned char* stage, T* xb,
                                              const T* __restrict__ x, int lane) {
-  int eend = S.e0;
-  for (int j = 0; j < S.ni; ++j) {
-    const Item I = S.items[j];
-    for (int c = lane; c < I.ncol; c += 32) cp_async(xb + I.xb + c, x + I.xo + c);
-    if (I.ne > 0) eend = max(eend, I.eb + (int)I.ne);
+  const ChunkHdr& H = *reinterpret_cast<const ChunkHdr*>(stage);
+  const Gather* ga = reinterpret_cast<const Gather*>(stage + H.o_gath);
+  for (int g = 0; g < H.ng; ++g) {
+    const Gather G = ga[g];
+    for (int i = lane; i < G.n; i += 32) cp_async(xb + G.dst + i, x + G.xs + i);
   }
-  T* xr = xb + S.ndx;
-  const int ne = eend - S.e0;
-  for (int e = lane; e < ne; e += 32) cp_async(xr + e, x + S.ridx[e]);
+  const int32_t* ri = reinterpret_cast<const int32_t*>(stage + H.o_ridx);
+  T* xr = xb + H.ndx;
+  for (int e = lane; e < H.nent; e += 32) cp_async(xr + e, x + ri[e]);
 }
 
-// The row sums of one item (lanes < nr hold rows row0 .. row0 + nr - 1).
 template <typename T>
-__device__ __forceinline__ T item_rows(const StageView<T>& S, const Item& I, const T* xb,
-                                       int lane) {
-  const int nr = I.nr, ncol = I.ncol, ne = I.ne;
-  // (1) dense slab
-  T acc = T(0);
-  if (ncol > 0) {
-    const int Q = I.q, active = Q * nr, ph = (lane * (int)I.qm) >> 15, row = lane - ph * nr;
-    if (lane < active) {
-      const T* vp = S.val + (I.voff - S.v0) + ph * nr + row;
+__device__ __forceinline__ void compute_chunk(const Plan<T>& P, const unsigned char* stage,
+                                              const T* xb, T* __restrict__ y, T& run, int lane) {
+  const ChunkHdr& H = *reinterpret_cast<const ChunkHdr*>(stage);
+  const SItem* items = reinterpret_cast<const SItem*>(stage + H.o_item);
+  const uint32_t* lmap = reinterpret_cast<const uint32_t*>(stage + H.o_lane);
+  const int32_t* rptr = reinterpret_cast<const int32_t*>(stage + H.o_rptr);
+  const T* val = reinterpret_cast<const T*>(stage + H.o_val);
+  const T* rval = reinterpret_cast<const T*>(stage + H.o_rval);
+  const T* xr = xb + H.ndx;
+  for (int b = 0; b < H.nb; ++b) {
+    const uint32_t m = lmap[b * 32 + lane];
+    const bool valid = (m & kLaneValid) != 0;
+    const int r = (m >> 8) & 31, ph = (m >> 13) & 31, lq = (m >> 18) & 7, Q = 1 << lq;
+    SItem I{};
+    if (valid) I = items[m & 255];
+    const int nr = I.nr;
+    T acc = T(0);
+    if (valid) {
+      // dense: columns ph, ph + Q, ... of row r (column-major slab, ld nr)
+      const T* vp = val + I.v + ph * nr + r;
       const T* xs = xb + I.xb;
-      const int stride = active;  // values between a lane's columns c and c + Q
+      const int step = Q * nr;
+      // two interleaved accumulators (columns 2j and 2j + 1 of the lane)
+      // for ILP; the order is fixed by the item alone
+      T acc1 = T(0);
       int c = ph;
-      for (; c + 3 * Q < ncol; c += 4 * Q) {
+      for (; c + 3 * Q < I.ncol; c += 4 * Q) {
         acc = fma(vp[0], xs[c], acc);
-        acc = fma(vp[stride], xs[c + Q], acc);
-        acc = fma(vp[2 * stride], xs[c + 2 * Q], acc);
-        acc = fma(vp[3 * stride], xs[c + 3 * Q], acc);
-        vp += 4 * stride;
+        acc1 = fma(vp[step], xs[c + Q], acc1);
+        acc = fma(vp[2 * step], xs[c + 2 * Q], acc);
+        acc1 = fma(vp[3 * step], xs[c + 3 * Q], acc1);
+        vp += 4 * step;
       }
-      for (; c < ncol; c += Q) {
+      for (; c < I.ncol; c += Q) {
         acc = fma(*vp, xs[c], acc);
-        vp += stride;
+        vp += step;
+      }
+      acc += acc1;
+      // remainder: entries ph, ph + Q, ... of row r within the item's entries
+      if (I.ne > 0) {
+        const int rr = I.row0 + r - H.r0;
+        const int e_lo = I.e, e_hi = I.e + I.ne;  // chunk-relative
+        const int lo = max(rptr[rr] - H.e0, e_lo), hi = min(rptr[rr + 1] - H.e0, e_hi);
+        for (int e = lo + ph; e < hi; e += Q) acc = fma(rval[e], xr[e], acc);
       }
     }
-    for (int off = 1; off < Q; off <<= 1) {
-      const T o = __shfl_down_sync(kFull, acc, off * nr);
-      if (lane < active && ph + off < Q) acc += o;
+    // fold the phases: lane ph * nr + r collects ph + 1, ph + 2, ... in order
+    // of a binary tree (fixed by Q and nr: deterministic)
+    const int lqmax = __reduce_max_sync(kFull, (unsigned)(valid ? lq : 0));
+    for (int l = 0; l < lqmax; ++l) {
+      const int d = (1 << l) * nr;
+      const T o = __shfl_sync(kFull, acc, min(lane + d, 31));
+      if (valid && ((ph >> l) & 1) == 0 && ph + (1 << l) < Q) acc += o;
+    }
+    if (valid && ph == 0) {
+      if (!(I.flags & IF_XG)) {
+        run = (I.flags & IF_FIRST) ? acc : run + acc;
+        if (I.flags & IF_LAST) y[I.row0 + r] += run;  // y holds the remainder part
+      }
+    }
+    // a piece of a group shared with another task (alone in its bundle, so
+    // lane 0 holds row 0 of it): meet in global scratch
+    if (__any_sync(kFull, valid && (I.flags & IF_XG))) {
+      const int nr0 = __shfl_sync(kFull, nr, 0), row0 = __shfl_sync(kFull, I.row0, 0);
+      const XgInfo xi = P.xgi[(int64_t)H.i0 + (lmap[b * 32] & 255)];
+      T* sp = P.scratch + xi.slot;
+      if (valid && ph == 0) __stcg(sp + xi.p * 32 + r, acc);
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = (atom_add_acq_rel(P.counters + xi.g, 1) + 1 == xi.npieces);
+      last = __shfl_sync(kFull, last, 0);
+      if (last) {
+        if (lane < nr0) {
+          T sum = __ldcg(sp + lane);
+          for (int q = 1; q < xi.npieces; ++q) sum += __ldcg(sp + q * 32 + lane);
+          y[row0 + lane] += sum;
+        }
+        if (lane == 0) P.counters[xi.g] = 0;  // ready for the next launch
+      }
     }
   }
-  // (2) remainder: lane r sums row r (the whole warp for long rows)
-  if (ne > 0) {
-    const int eo = I.eb - S.e0;
-    const T* rv = S.rval + eo;
-    const T* xr = xb + S.ndx + eo;
-    int lo = 0, hi = 0;
-    if (lane < nr) {
-      const int rr = I.row0 + lane - S.r0;
-      lo = max(S.rptr[rr], I.eb) - I.eb;
-      hi = min(S.rptr[rr + 1], I.eb + ne) - I.eb;
-      if (hi < lo) hi = lo;
-    }
-    T racc = T(0);
-    const bool longr = (hi - lo) > kLongRow;
-    unsigned lm = __ballot_sync(kFull, longr);
-    if (!longr)
-      for (int e = lo; e < hi; ++e) racc = fma(rv[e], xr[e], racc);
-    while (lm) {
-      const int r = __ffs(lm) - 1;
-      lm &= lm - 1;
-      const int l2 = __shfl_sync(kFull, lo, r), h2 = __shfl_sync(kFull, hi, r);
-      T sum = T(0);
-      for (int e = l2 + lane; e < h2; e += 32) sum = fma(rv[e], xr[e], sum);
-      sum = warp_sum(sum);
-      if (lane == r) racc = sum;
-    }
-    acc += racc;
-  }
-  return acc;
 }
 
 // ---------------------------------------------------------------- kernel
@@ -264,22 +236,18 @@ __global__ void __launch_bounds__(kThreads)
   const int NS = P.nstage;
   unsigned char* ws =
       smem + (size_t)warp * warp_smem_bytes(NS, P.stage_bytes, P.xbuf, (int)sizeof(T));
-  uint64_t* full = reinterpret_cast<uint64_t*>(ws);     // [kMaxStages]
-  Chunk* cdesc = reinterpret_cast<Chunk*>(ws + 64);     // [kMaxStages]
-  T* xbuf = reinterpret_cast<T*>(ws + 512);             // [2][P.xbuf]
-  unsigned char* stages = ws + 512 + ((2 * P.xbuf * (int)sizeof(T) + 127) & ~127);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ws);  // [kMaxStages]
+  T* xbuf = reinterpret_cast<T*>(ws + 256);          // [2][P.xbuf]
+  unsigned char* stages = ws + 256 + ((2 * P.xbuf * (int)sizeof(T) + 127) & ~127);
 
   uint64_t pol = 0;
   if (lane == 0) {
     pol = policy_evict_first();
     for (int s = 0; s < NS; ++s) mbar_init(smem_u32(full + s), 1);
     fence_barrier_init();
-    for (int s = 0; s < NS && kb + s < ke; ++s) {
-      const Chunk c = P.chunks[kb + s];
-      cdesc[s] = c;
-      issue_chunk(P, c, kb + s + NS < ke ? kb + s + NS : -1, stages + (size_t)s * P.stage_bytes,
+    for (int s = 0; s < NS && kb + s < ke; ++s)
+      issue_chunk(P.stream, P.cref[kb + s], stages + (size_t)s * P.stage_bytes,
                   smem_u32(full + s), pol);
-    }
   }
   __syncwarp();
 
@@ -288,10 +256,9 @@ __global__ void __launch_bounds__(kThreads)
   int s = 0, b = 0;
   uint32_t phase = 0;
   mbar_wait(smem_u32(full + 0), 0);
-  StageView<T> S = stage_view<T>(stages, cdesc[0]);
-  if (P.mode != 1) gather_chunk(S, xbuf, x, lane);
+  if (P.mode != 1) gather_chunk(stages, xbuf, x, lane);
   cp_async_commit();
-  T run = T(0);  // running sum of the current group's pieces (lanes < nr)
+  T run = T(0);  // running sum of a split group's pieces (lanes < nr)
   for (int64_t k = kb; k < ke; ++k) {
     int sn = s + 1;
     uint32_t phn = phase;
@@ -299,55 +266,25 @@ __global__ void __launch_bounds__(kThreads)
       sn = 0;
       phn ^= 1u;
     }
-    StageView<T> Sn = S;
+    unsigned char* stage = stages + (size_t)s * P.stage_bytes;
     if (k + 1 < ke) {
+      unsigned char* nst = stages + (size_t)sn * P.stage_bytes;
       mbar_wait(smem_u32(full + sn), phn);
-      Sn = stage_view<T>(stages + (size_t)sn * P.stage_bytes, cdesc[sn]);
-      if (P.mode != 1) gather_chunk(Sn, xbuf + (b ^ 1) * P.xbuf, x, lane);
+      if (P.mode != 1) gather_chunk(nst, xbuf + (b ^ 1) * P.xbuf, x, lane);
     }
     cp_async_commit();
     cp_async_wait<1>();  // chunk k's x
     __syncwarp();
-    if (P.mode != 1) {
-      const T* xb = xbuf + b * P.xbuf;
-      for (int j = 0; j < S.ni; ++j) {
-        const Item I = S.items[j];
-        const T tot = item_rows(S, I, xb, lane);
-        if (!(I.flags & IF_XG)) {
-          run = (I.flags & IF_FIRST) ? tot : run + tot;
-          if ((I.flags & IF_LAST) && lane < I.nr) y[I.row0 + lane] = run;
-        } else {
-          // a group shared with another task: meet in global scratch
-          const XgInfo xi = P.xgi[(int64_t)cdesc[s].i0 + j];
-          T* sp = P.scratch + xi.slot;
-          if (lane < I.nr) __stcg(sp + xi.p * 32 + lane, tot);
-          __syncwarp();
-          int last = 0;
-          if (lane == 0) last = (atom_add_acq_rel(P.counters + xi.g, 1) + 1 == xi.npieces);
-          last = __shfl_sync(kFull, last, 0);
-          if (last) {
-            if (lane < I.nr) {
-              T sum = __ldcg(sp + lane);
-              for (int q = 1; q < xi.npieces; ++q) sum += __ldcg(sp + q * 32 + lane);
-              y[I.row0 + lane] = sum;
-            }
-            if (lane == 0) P.counters[xi.g] = 0;  // ready for the next launch
-          }
-        }
-      }
-    }
-    // refill this stage with chunk k + NS (its descriptor rode in with chunk k)
+    if (P.mode != 1) compute_chunk(P, stage, xbuf + b * P.xbuf, y, run, lane);
+    // refill this stage with the chunk nstage ahead (named by this header)
     __syncwarp();
-    if (lane == 0 && k + NS < ke) {
-      unsigned char* stage = stages + (size_t)s * P.stage_bytes;
-      const Chunk nd = *reinterpret_cast<const Chunk*>(stage);
-      cdesc[s] = nd;
-      issue_chunk(P, nd, k + 2 * NS < ke ? k + 2 * NS : -1, stage, smem_u32(full + s), pol);
+    if (lane == 0) {
+      const ChunkRef nx = reinterpret_cast<const ChunkHdr*>(stage)->next;
+      if (nx.bytes > 0) issue_chunk(P.stream, nx, stage, smem_u32(full + s), pol);
     }
     __syncwarp();
     s = sn;
     phase = phn;
-    S = Sn;
     b ^= 1;
   }
   cp_async_wait<0>();
@@ -364,14 +301,10 @@ template <typename T>
 cudaError_t launch_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st) {
   if (h->n_chunks == 0) return cudaSuccess;
   Plan<T> P;
-  P.chunks = h->chunks;
+  P.stream = h->stream;
+  P.cref = h->cref;
   P.task = h->task;
-  P.items = h->items;
   P.xgi = h->xgi;
-  P.tval = static_cast<const T*>(h->tval);
-  P.rem_ptr = h->rem_ptr;
-  P.rem_idx = h->rem_idx;
-  P.rem_val = static_cast<const T*>(h->rem_val);
   P.scratch = static_cast<T*>(h->scratch);
   P.counters = h->counters;
   P.n_tasks = h->cfg.n_tasks;
@@ -394,7 +327,16 @@ cudaError_t launch_spmv(const sable_handle* h, const void* x, void* y, cudaStrea
   return cudaGetLastError();
 }
 
+template <typename T>
+cudaError_t launch_rem(const sable_handle* h, const void* x, void* y, cudaStream_t st);
+
+// y = A x: the remainder executor writes every local row (its remainder
+// sum, or 0), then the dense-tile executor adds the dense part of the rows
+// of block rows with tiles.
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st) {
+  cudaError_t e = h->dtype == SABLE_F64 ? launch_rem<double>(h, x, y, st)
+                                        : launch_rem<float>(h, x, y, st);
+  if (e != cudaSuccess) return e;
   return h->dtype == SABLE_F64 ? launch_spmv<double>(h, x, y, st)
                                : launch_spmv<float>(h, x, y, st);
 }

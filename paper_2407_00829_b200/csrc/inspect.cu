@@ -517,12 +517,15 @@ int64_t env_int(const char* name, int64_t dflt) {
 
 // ------------------------------------------------------------------- a5: plan
 
+int64_t g_lane_work = 48;  // SABLE_LANE_WORK (plan-time tuning; see item_lq)
+
 // Executor shape; SABLE_* environment variables override the defaults
 // (tuning and tests).  Invalid overrides -> SABLE_E_INVALID_ARG.
 ExecCfg exec_config(int sv) {
   ExecCfg c;
+  // defaults: the best of the r01 sweeps on B200 (C2 / C3 / C4)
   c.stage_bytes = (int32_t)env_int("SABLE_STAGE_BYTES", 3072);
-  c.nstage = (int32_t)env_int("SABLE_NSTAGE", 3);
+  c.nstage = (int32_t)env_int("SABLE_NSTAGE", 2);
   c.item_bytes = (int32_t)env_int("SABLE_ITEM_BYTES", c.stage_bytes - 512);
   c.xbuf = (int32_t)env_int("SABLE_XBUF", 384);
   const int64_t per_cta = (int64_t)kWarps * warp_smem_bytes(c.nstage, c.stage_bytes, c.xbuf, sv);
@@ -530,11 +533,11 @@ ExecCfg exec_config(int sv) {
       "SABLE_CTAS_PER_SM", std::max<int64_t>(1, std::min<int64_t>(8, (227 * 1024) / per_cta)));
   c.mode = (int32_t)env_int("SABLE_EXEC_MODE", 0);
   c.n_tasks = (int32_t)env_int("SABLE_TASKS", 0);  // 0 = one per executor warp
-  const bool ok = c.stage_bytes % 128 == 0 && c.stage_bytes <= 65536 && c.nstage >= 2 &&
-                  c.nstage <= kMaxStages && c.item_bytes >= 4 * sv &&
-                  c.item_bytes + 256 <= c.stage_bytes && c.xbuf >= 64 && c.xbuf <= 16384 &&
-                  c.ctas_per_sm >= 1 &&
-                  per_cta * c.ctas_per_sm <= 227 * 1024 && c.n_tasks >= 0;
+  g_lane_work = std::max<int64_t>(1, env_int("SABLE_LANE_WORK", 48));
+  const bool ok = c.stage_bytes % 128 == 0 && c.stage_bytes >= 1024 && c.stage_bytes <= 65536 &&
+                  c.nstage >= 2 && c.nstage <= kMaxStages && c.item_bytes >= 8 * sv &&
+                  c.item_bytes + 512 <= c.stage_bytes && c.xbuf >= 32 && c.xbuf <= 32768 &&
+                  c.ctas_per_sm >= 1 && per_cta * c.ctas_per_sm <= 227 * 1024 && c.n_tasks >= 0;
   if (!ok) {
     set_error("invalid SABLE_STAGE_BYTES / SABLE_NSTAGE / SABLE_ITEM_BYTES / SABLE_XBUF / "
               "SABLE_CTAS_PER_SM / SABLE_TASKS combination");
@@ -550,10 +553,73 @@ int device_sms() {
   return n > 0 ? n : 148;
 }
 
-// Work items (row groups or pieces of them) and warp tasks (contiguous item
-// ranges of about equal bytes, one per executor warp).  Items depend only on
-// the block rows, and a group's pieces are summed left to right whoever
-// processes them, so y is identical for every shard count.
+// Per chunk, for the stream packer.
+struct PackDesc {
+  int64_t soff;      // stream offset of the chunk
+  int64_t meta_src;  // offset of its metadata image in the upload buffer
+  int64_t v_lo;      // first dense value
+  int32_t meta_bytes, o_rptr, o_val, o_ridx, o_rval;
+  int32_t nv, r_lo, nrow1, e_lo, nent;
+};
+
+// One CTA per chunk: metadata image, row pointers, values, remainder.
+template <typename T>
+__global__ void k_pack_stream(const PackDesc* pd, const unsigned char* meta, const int32_t* rem_ptr,
+                              const T* tval, const int32_t* ridx, const T* rval,
+                              unsigned char* stream) {
+  const PackDesc d = pd[blockIdx.x];
+  unsigned char* dst = stream + d.soff;
+  const uint32_t* ms = reinterpret_cast<const uint32_t*>(meta + d.meta_src);
+  uint32_t* md = reinterpret_cast<uint32_t*>(dst);
+  for (int i = threadIdx.x; i < d.meta_bytes / 4; i += blockDim.x) md[i] = ms[i];
+  int32_t* rp = reinterpret_cast<int32_t*>(dst + d.o_rptr);
+  for (int i = threadIdx.x; i < d.nrow1; i += blockDim.x) rp[i] = rem_ptr[d.r_lo + i];
+  T* vv = reinterpret_cast<T*>(dst + d.o_val);
+  for (int i = threadIdx.x; i < d.nv; i += blockDim.x) vv[i] = tval[d.v_lo + i];
+  int32_t* ri = reinterpret_cast<int32_t*>(dst + d.o_ridx);
+  T* rv = reinterpret_cast<T*>(dst + d.o_rval);
+  for (int i = threadIdx.x; i < d.nent; i += blockDim.x) {
+    ri[i] = ridx[d.e_lo + i];
+    rv[i] = rval[d.e_lo + i];
+  }
+}
+
+inline int64_t al16(int64_t v) { return (v + 15) & ~(int64_t)15; }
+
+// Plan-time work item.
+struct HItem {
+  int64_t voff, eb, xp;
+  int32_t ne, ncol, row0, nr, maxrow, nseg;
+  int32_t g, p, np;
+  uint8_t flags;
+};
+
+// Bundle lane maps.  Item i gets Q_i = 2^lq_i phases: the smallest power of
+// two with ceil(w_i / Q_i) <= lane work (w_i = its columns + its longest
+// remainder row) and nr_i * Q_i <= 32.  Q_i depends on the item alone, so a
+// row's summation order never depends on how items are packed into bundles
+// (or on the shard); bundles only pack items with sum_i nr_i * Q_i <= 32.
+
+struct BundleState {
+  std::vector<int> nr, lq;
+  int lanes = 0;
+  int64_t maxw = 0;
+  bool single = false;  // a split-group piece: alone, lane = ph * nr + r
+};
+
+int item_lq(int nr, int64_t w) {
+  int lq = 0;
+  while (((w + (1ll << lq) - 1) >> lq) > g_lane_work && (nr << (lq + 1)) <= 32) ++lq;
+  return lq;
+}
+
+constexpr int64_t kBundleOverhead = 8;  // fixed cost of a bundle, in lane-steps
+
+// Work items (row groups or pieces of groups larger than a stage), chunks
+// (one stage each), bundles (lane maps) and warp tasks (contiguous chunk
+// ranges of about equal bytes), then the packed executor stream.  Items
+// depend only on the block rows and a group's pieces are summed left to
+// right whoever processes them, so y is identical for every shard count.
 template <typename T>
 void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
                    const std::vector<int32_t>& H_rpntr, const std::vector<int32_t>& H_W,
@@ -578,12 +644,24 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
                                       [](int64_t v, const XTile& t) { return v < (int64_t)t.tp; }) -
                      R.begin() - 1);
   };
+  auto nseg_of = [&](int64_t xp, int64_t ncol) -> int32_t {
+    if (ncol <= 0) return 0;
+    return (int32_t)(run_of(xp + ncol - 1) - run_of(xp) + 1);
+  };
+  auto maxrow_of = [&](int32_t row0, int nr, int64_t e0, int64_t e1) {
+    int32_t m = 0;
+    for (int r = 0; r < nr; ++r) {
+      const int64_t lo = std::max<int64_t>(H_rp[row0 + r], e0), hi = std::min<int64_t>(H_rp[row0 + r + 1], e1);
+      m = std::max<int32_t>(m, (int32_t)std::max<int64_t>(0, hi - lo));
+    }
+    return m;
+  };
 
-  std::vector<Item> It;
-  std::vector<XgInfo> Xg;
-  std::vector<int64_t> Ib;  // streamed bytes per item
+  // ---- items
+  std::vector<HItem> It;
   It.reserve((size_t)(H_rp.size() / 8 + nbl + 1));
   int64_t slot = 0, ngroups = 0;
+  const int64_t xcap = cfg.xbuf;
   for (int32_t la = 0; la < nbl; ++la) {
     const int32_t a = b0 + la;
     const int32_t hgt = H_rpntr[a + 1] - H_rpntr[a];
@@ -591,188 +669,167 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
     const int32_t r0 = (int32_t)(H_rpntr[a] - h->row_begin);
     const int64_t xp = br_wprefix[la];
     for (int32_t j = 0; j * kGroupRows < hgt; ++j) {
-      Item base{};
+      HItem base{};
       base.row0 = r0 + j * kGroupRows;
-      const int nr = std::min(kGroupRows, hgt - j * kGroupRows);
-      base.nr = (uint8_t)nr;
-      base.q = (uint8_t)(32 / nr);
-      base.qm = (uint16_t)(32768 / nr + 1);
+      base.nr = std::min(kGroupRows, hgt - j * kGroupRows);
+      base.g = (int32_t)ngroups;
       const int64_t voff = br_vbase[la] + (int64_t)j * kGroupRows * W;
-      const int64_t eb = H_rp[base.row0], ee = H_rp[base.row0 + nr];
-      const int64_t dbytes = W * nr * sv, rbytes = (ee - eb) * (sv + 4);
+      // the remainder has its own executor (rem.cu): items carry dense work
+      // only, and block rows without tiles have no items
+      if (W == 0) continue;
+      const int64_t eb = H_rp[base.row0], ee = eb;
+      const int64_t meta = 16 + 8 + 4 * (base.nr + 1) + 8 * nseg_of(xp, W);
+      const int64_t bytes = W * base.nr * sv + (ee - eb) * (sv + 4) + meta;
       const size_t first = It.size();
-      const int64_t k0 = W > 0 ? run_of(xp) : 0;
-      const bool one_run = W == 0 || (int64_t)R[k0 + 1].tp >= xp + W;
-      if (one_run && dbytes + rbytes + 32 <= cap && ee - eb <= kRE && W + (ee - eb) <= cfg.xbuf) {
-        Item it = base;
+      if (bytes <= cap && W + (ee - eb) <= xcap && ee - eb <= 65535) {
+        HItem it = base;
         it.voff = voff;
-        it.eb = (int32_t)eb;
-        it.ne = (int16_t)(ee - eb);
-        it.ncol = (int16_t)W;
-        it.xo = W > 0 ? (int32_t)(R[k0].c0 - R[k0].tp + xp) : 0;
+        it.eb = eb;
+        it.ne = (int32_t)(ee - eb);
+        it.ncol = (int32_t)W;
+        it.xp = xp;
         It.push_back(it);
-        Ib.push_back(dbytes + rbytes + 32);
       } else {
-        // dense pieces: column ranges inside one run, <= cap bytes each
-        const int64_t dc = std::max<int64_t>(
-            1, std::min<int64_t>(cfg.xbuf, (cap - 32) / (nr * sv)));
-        int64_t c = 0, k = k0;
+        // pieces: column ranges (each <= cap bytes incl. its x segments), then entry ranges
+        int64_t c = 0;
         while (c < W) {
-          const int64_t run_end = std::min<int64_t>(W, (int64_t)R[k + 1].tp - xp);
-          const int64_t ce = std::min(run_end, c + dc);
-          Item it = base;
-          it.voff = voff + c * nr;
-          it.eb = (int32_t)ee;
-          it.ncol = (int16_t)(ce - c);
-          it.xo = (int32_t)(R[k].c0 - R[k].tp + xp + c);
+          int64_t n = std::max<int64_t>(1, std::min<int64_t>(xcap, (cap - 64) / (base.nr * sv + 8)));
+          n = std::min(n, W - c);
+          HItem it = base;
+          it.voff = voff + c * base.nr;
+          it.eb = ee;
+          it.ncol = (int32_t)n;
+          it.xp = xp + c;
           It.push_back(it);
-          Ib.push_back((ce - c) * nr * sv + 32);
-          c = ce;
-          if (c >= run_end) ++k;
+          c += n;
         }
-        const int64_t rc = std::max<int64_t>(
-            1, std::min<int64_t>(std::min<int64_t>(kRE, cfg.xbuf), (cap - 32) / (sv + 4)));
+        const int64_t rc = std::max<int64_t>(1, std::min<int64_t>(xcap, (cap - 64 - 4 * (base.nr + 1)) / (sv + 4)));
         for (int64_t e = eb; e < ee; e += rc) {
-          Item it = base;
+          HItem it = base;
           it.voff = voff;
-          it.eb = (int32_t)e;
-          it.ne = (int16_t)(std::min(ee, e + rc) - e);
+          it.eb = e;
+          it.ne = (int32_t)(std::min(ee, e + rc) - e);
           It.push_back(it);
-          Ib.push_back(it.ne * (sv + 4) + 32);
         }
-        if (It.size() == first) {
-          It.push_back(base);
-          Ib.push_back(32);
-        }
+        if (It.size() == first) It.push_back(base);
       }
-      const int64_t np = (int64_t)(It.size() - first);
+      const int32_t np = (int32_t)(It.size() - first);
       for (size_t q = first; q < It.size(); ++q) {
-        It[q].flags = (uint8_t)((q == first ? IF_FIRST : 0) | (q + 1 == It.size() ? IF_LAST : 0));
-        XgInfo xi{};
-        xi.slot = np > 1 ? slot : 0;
-        xi.g = (int32_t)ngroups;
-        xi.p = (int16_t)std::min<int64_t>(q - first, 32767);
-        xi.npieces = (int32_t)np;
-        Xg.push_back(xi);
+        HItem& it = It[q];
+        it.flags = (uint8_t)((q == first ? IF_FIRST : 0) | (q + 1 == It.size() ? IF_LAST : 0));
+        it.p = (int32_t)(q - first);
+        it.np = np;
+        it.nseg = nseg_of(it.xp, it.ncol);
+        it.maxrow = it.ne > 0 ? maxrow_of(it.row0, it.nr, it.eb, it.eb + it.ne) : 0;
       }
-      if (np > 32767) {
-        set_error("a row group needs more than 32767 work items");
-        throw Fail{SABLE_E_UNSUPPORTED};
-      }
-      if (np > 1) slot += np * kGroupRows;
+      if (np > 1) slot += (int64_t)np * kGroupRows;
       ++ngroups;
     }
   }
   const int64_t nit = (int64_t)It.size();
 
-  // chunks: greedy runs of consecutive items whose five ranges (items, row
-  // pointers, values, remainder columns, remainder values; each rounded out
-  // to 16 bytes) fit one stage after the 64-byte descriptor slot
-  struct Acc {
-    int64_t i0 = 0, ni = 0, vlo = 0, vhi = 0, elo = 0, ehi = 0, rlo = 0, rhi = 0, ndx = 0;
+  // ---- chunks (greedy: consecutive items that fit a stage) with bundles
+  struct CAcc {
+    int64_t i0 = 0, ni = 0, vlo = 0, vhi = 0, elo = 0, ehi = 0, rlo = 0, rhi = 0;
+    int64_t ndx = 0, ng = 0;
     bool dv = false, de = false;
+    std::vector<BundleState> B;
+    std::vector<int64_t> bitem;  // first item (chunk-relative) of each bundle
   };
-  auto extend = [&](Acc A, int64_t i) {
-    const Item& it = It[i];
+  auto chunk_bytes = [&](const CAcc& A) {
+    const int64_t o_rptr = al16(64 + 16 * A.ni + 128 * (int64_t)A.B.size() + 8 * A.ng);
+    const int64_t nent = A.de ? A.ehi - A.elo : 0;
+    return o_rptr + al16(4 * (A.de ? A.rhi - A.rlo + 1 : 0)) + al16(sv * (A.dv ? A.vhi - A.vlo : 0)) +
+           al16(4 * nent) + al16(sv * nent);
+  };
+  auto fits = [&](const CAcc& A) {
+    const int64_t nent = A.de ? A.ehi - A.elo : 0;
+    return chunk_bytes(A) <= cfg.stage_bytes && A.ndx + nent <= xcap && A.ni <= 255 &&
+           nent <= 65535;
+  };
+  auto add_item = [&](CAcc A, int64_t i) {
+    const HItem& it = It[i];
     if (A.ni == 0) A.i0 = i;
+    const int64_t rel = A.ni;
     A.ni++;
     A.ndx += it.ncol;
+    A.ng += it.nseg;
     if (it.ncol > 0) {
       const int64_t v0 = it.voff, v1 = it.voff + (int64_t)it.ncol * it.nr;
       if (!A.dv) { A.vlo = v0; A.vhi = v1; A.dv = true; }
       else { A.vlo = std::min(A.vlo, v0); A.vhi = std::max(A.vhi, v1); }
     }
     if (it.ne > 0) {
-      const int64_t e0 = it.eb, e1 = (int64_t)it.eb + it.ne;
+      const int64_t e0 = it.eb, e1 = it.eb + it.ne;
       if (!A.de) { A.elo = e0; A.ehi = e1; A.rlo = it.row0; A.rhi = it.row0 + it.nr; A.de = true; }
       else {
         A.elo = std::min(A.elo, e0); A.ehi = std::max(A.ehi, e1);
         A.rlo = std::min<int64_t>(A.rlo, it.row0); A.rhi = std::max<int64_t>(A.rhi, it.row0 + it.nr);
       }
     }
+    // bundle: split-group pieces alone (canonical map); otherwise join the
+    // open bundle if its lanes allow and the lanes' work does not grow much
+    const int64_t w = (int64_t)it.ncol + it.maxrow;
+    const bool single = it.np > 1;
+    int lq = item_lq(it.nr, w);
+    if (single)  // canonical map: Q = 32 / nr phases, lane = ph * nr + r
+      while ((it.nr << (lq + 1)) <= 32) ++lq;
+    const int64_t wl = (w + (1ll << lq) - 1) >> lq;
+    bool merged = false;
+    if (!single && !A.B.empty() && !A.B.back().single) {
+      BundleState& M = A.B.back();
+      if (M.lanes + (it.nr << lq) <= 32 && wl <= 2 * M.maxw + kBundleOverhead &&
+          M.maxw <= 2 * wl + kBundleOverhead) {
+        M.nr.push_back(it.nr);
+        M.lq.push_back(lq);
+        M.lanes += it.nr << lq;
+        M.maxw = std::max(M.maxw, wl);
+        merged = true;
+      }
+    }
+    if (!merged) {
+      BundleState S1;
+      S1.nr = {it.nr};
+      S1.lq = {lq};
+      S1.lanes = it.nr << lq;
+      S1.maxw = wl;
+      S1.single = single;
+      A.B.push_back(S1);
+      A.bitem.push_back(rel);
+    }
     return A;
   };
-  struct Rng { int64_t first, count; int es; };
-  auto ranges = [&](const Acc& A, Rng* r) {
-    r[SR_ITEM] = {A.i0, A.ni, (int)sizeof(Item)};
-    r[SR_RPTR] = {A.rlo, A.de ? A.rhi - A.rlo + 1 : 0, 4};
-    r[SR_VAL] = {A.vlo, A.dv ? A.vhi - A.vlo : 0, (int)sv};
-    r[SR_RIDX] = {A.elo, A.de ? A.ehi - A.elo : 0, 4};
-    r[SR_RVAL] = {A.elo, A.de ? A.ehi - A.elo : 0, (int)sv};
-  };
-  auto bytes_of = [&](const Acc& A) {
-    if (A.ndx + (A.de ? A.ehi - A.elo : 0) > cfg.xbuf || A.ni > 32767)
-      return (int64_t)cfg.stage_bytes + 1;  // the chunk's x would not fit the buffer
-    Rng r[SR_N];
-    ranges(A, r);
-    int64_t o = 64;
-    for (int k = 0; k < SR_N; ++k) {
-      if (r[k].count <= 0) continue;
-      const int64_t a0 = r[k].first * r[k].es, a1 = a0 + r[k].count * r[k].es;
-      o += ((a1 + 15) & ~(int64_t)15) - (a0 & ~(int64_t)15);
-    }
-    return o;
-  };
-  std::vector<Chunk> Ch;
-  std::vector<int64_t> Cb;
-  auto push = [&](const Acc& A) {
-    Rng r[SR_N];
-    ranges(A, r);
-    Chunk c{};
-    int64_t o = 64;
-    for (int k = 0; k < SR_N; ++k) {
-      if (r[k].count <= 0) continue;
-      const int64_t a0 = r[k].first * r[k].es, a1 = a0 + r[k].count * r[k].es;
-      const int64_t A0 = a0 & ~(int64_t)15, A1 = (a1 + 15) & ~(int64_t)15;
-      c.src16[k] = (uint32_t)(A0 / 16);
-      c.bytes[k] = (uint16_t)(A1 - A0);
-      c.off[k] = (uint16_t)(o + (a0 - A0));
-      o += A1 - A0;
-    }
-    c.v0 = A.vlo;
-    c.e0 = (int32_t)A.elo;
-    c.r0 = (int32_t)A.rlo;
-    c.ni = (int16_t)A.ni;
-    c.ndx = (int16_t)A.ndx;
-    c.i0 = (int32_t)A.i0;
-    int64_t xb = 0;
-    for (int64_t q = A.i0; q < A.i0 + A.ni; ++q) {
-      It[q].xb = (int16_t)xb;
-      xb += It[q].ncol;
-    }
-    Ch.push_back(c);
-    Cb.push_back(o);
-  };
+
+  std::vector<CAcc> Ch;
   {
-    Acc cur;
+    CAcc cur;
     for (int64_t i = 0; i < nit; ++i) {
-      Acc nxt = extend(cur, i);
-      if (cur.ni > 0 && bytes_of(nxt) > cfg.stage_bytes) {
-        push(cur);
-        nxt = extend(Acc{}, i);
+      CAcc nxt = add_item(cur, i);
+      if (cur.ni > 0 && !fits(nxt)) {
+        Ch.push_back(std::move(cur));
+        nxt = add_item(CAcc{}, i);
       }
-      if (bytes_of(nxt) > cfg.stage_bytes) {
+      if (!fits(nxt)) {
         set_error("internal: a work item does not fit one executor stage");
         throw Fail{SABLE_E_UNSUPPORTED};
       }
-      cur = nxt;
+      cur = std::move(nxt);
     }
-    if (cur.ni > 0) push(cur);
+    if (cur.ni > 0) Ch.push_back(std::move(cur));
   }
   const int64_t nch = (int64_t)Ch.size();
-  if (nch > 0 && (int64_t)(It.size() * sizeof(Item)) / 16 > (int64_t)UINT32_MAX) {
-    set_error("executor arrays exceed the 64 GiB bulk-copy offset range");
-    throw Fail{SABLE_E_UNSUPPORTED};
-  }
 
-  // warp tasks: contiguous chunk ranges of about equal bytes; a cut moves to
-  // the next group boundary when one is near, so only groups larger than a
+  // ---- warp tasks: contiguous chunk ranges of about equal bytes; a cut moves
+  // to the next group boundary when one is near, so only groups larger than a
   // fraction of a task are shared between warps (and combined in scratch)
   const int64_t grid = (int64_t)device_sms() * cfg.ctas_per_sm;
   const int64_t ntask = cfg.n_tasks > 0 ? cfg.n_tasks : std::max<int64_t>(1, grid * kWarps);
   cfg.n_tasks = (int32_t)ntask;
-  std::vector<int64_t> cpre(nch + 1, 0);
-  for (int64_t k = 0; k < nch; ++k) cpre[k + 1] = cpre[k] + Cb[k];
+  std::vector<int64_t> cbytes(nch), cpre(nch + 1, 0);
+  for (int64_t k = 0; k < nch; ++k) {
+    cbytes[k] = (chunk_bytes(Ch[k]) + 127) & ~(int64_t)127;
+    cpre[k + 1] = cpre[k] + cbytes[k];
+  }
   std::vector<int32_t> task(ntask + 1, 0);
   auto starts_group = [&](int64_t k) { return (It[Ch[k].i0].flags & IF_FIRST) != 0; };
   {
@@ -789,38 +846,214 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
     }
     task[ntask] = (int32_t)nch;
   }
-  // groups with pieces in more than one task combine through global scratch
-  for (int64_t t = 1; t < ntask; ++t) {
+  for (int64_t t = 1; t < ntask; ++t) {  // groups cut by a task boundary
     const int64_t k = task[t];
     if (k <= 0 || k >= nch) continue;
-    const int64_t i = Ch[k].i0;
-    if (It[i].flags & IF_FIRST) continue;
-    int64_t g0 = i;
+    int64_t g0 = Ch[k].i0;
+    if (It[g0].flags & IF_FIRST) continue;
     while (!(It[g0].flags & IF_FIRST)) --g0;
-    for (int64_t q = g0; q < g0 + Xg[g0].npieces; ++q) It[q].flags |= IF_XG;
+    for (int64_t q = g0; q < g0 + It[g0].np; ++q) It[q].flags |= IF_XG;
+  }
+  std::vector<int32_t> task_of(nch, 0);
+  for (int64_t t = 0; t < ntask; ++t)
+    for (int64_t k = task[t]; k < task[t + 1]; ++k) task_of[k] = (int32_t)t;
+
+  // ---- metadata images and pack descriptors
+  std::vector<ChunkRef> cref(nch);
+  for (int64_t k = 0; k < nch; ++k) cref[k] = ChunkRef{cpre[k], (int32_t)chunk_bytes(Ch[k]), 0};
+  std::vector<unsigned char> meta;
+  std::vector<PackDesc> pd(nch);
+  std::vector<XgInfo> Xg(nit);
+  for (int64_t k = 0; k < nch; ++k) {
+    const CAcc& A = Ch[k];
+    const int64_t nb = (int64_t)A.B.size();
+    ChunkHdr hd{};
+    const int64_t kn = k + cfg.nstage;
+    hd.next = (kn < nch && task_of[kn] == task_of[k]) ? cref[kn] : ChunkRef{0, 0, 0};
+    hd.o_item = 64;
+    hd.o_lane = (uint16_t)(64 + 16 * A.ni);
+    hd.o_gath = (uint16_t)(hd.o_lane + 128 * nb);
+    hd.o_rptr = (uint16_t)al16(hd.o_gath + 8 * A.ng);
+    const int64_t nrow1 = A.de ? A.rhi - A.rlo + 1 : 0, nv = A.dv ? A.vhi - A.vlo : 0;
+    const int64_t nent = A.de ? A.ehi - A.elo : 0;
+    hd.o_val = (uint16_t)(hd.o_rptr + al16(4 * nrow1));
+    hd.o_ridx = (uint16_t)(hd.o_val + al16(sv * nv));
+    hd.o_rval = (uint16_t)(hd.o_ridx + al16(4 * nent));
+    hd.ni = (uint16_t)A.ni;
+    hd.nb = (uint16_t)nb;
+    hd.ng = (uint16_t)A.ng;
+    hd.ndx = (uint16_t)A.ndx;
+    hd.r0 = (int32_t)A.rlo;
+    hd.e0 = (int32_t)A.elo;
+    hd.nent = (int32_t)nent;
+    hd.i0 = (int32_t)A.i0;
+    const size_t mstart = meta.size();
+    meta.resize(mstart + hd.o_rptr, 0);
+    unsigned char* m = meta.data() + mstart;
+    memcpy(m, &hd, sizeof(hd));
+    SItem* si = reinterpret_cast<SItem*>(m + hd.o_item);
+    Gather* ga = reinterpret_cast<Gather*>(m + hd.o_gath);
+    int64_t xb = 0, gi = 0;
+    for (int64_t q = 0; q < A.ni; ++q) {
+      const HItem& it = It[A.i0 + q];
+      SItem s{};
+      s.v = (uint16_t)(it.ncol > 0 ? it.voff - A.vlo : 0);
+      s.e = (uint16_t)(it.ne > 0 ? it.eb - A.elo : 0);
+      s.ne = (uint16_t)it.ne;
+      s.ncol = (uint16_t)it.ncol;
+      s.row0 = it.row0;
+      s.xb = (uint16_t)xb;
+      s.nr = (uint8_t)it.nr;
+      s.flags = it.flags;
+      si[q] = s;
+      // x gather segments: the runs under the item's columns
+      for (int64_t c = 0; c < it.ncol;) {
+        const int64_t r = run_of(it.xp + c);
+        const int64_t end = std::min<int64_t>(it.ncol, (int64_t)R[r + 1].tp - it.xp);
+        ga[gi++] = Gather{(int32_t)(R[r].c0 - R[r].tp + it.xp + c), (uint16_t)(end - c),
+                          (uint16_t)(xb + c)};
+        c = end;
+      }
+      xb += it.ncol;
+    }
+    // lane maps
+    uint32_t* lm = reinterpret_cast<uint32_t*>(m + hd.o_lane);
+    for (int64_t b = 0; b < nb; ++b) {
+      const BundleState& Bs = A.B[b];
+      int lane = 0;
+      for (size_t q = 0; q < Bs.nr.size(); ++q) {
+        const int item = (int)(A.bitem[b] + q), nr = Bs.nr[q], lq = Bs.lq[q];
+        for (int ph = 0; ph < (1 << lq); ++ph)
+          for (int r = 0; r < nr; ++r)
+            lm[b * 32 + lane++] = (uint32_t)item | (uint32_t)r << 8 | (uint32_t)ph << 13 |
+                                  (uint32_t)lq << 18 | kLaneValid;
+      }
+      for (; lane < 32; ++lane) lm[b * 32 + lane] = 0;
+    }
+    PackDesc d{};
+    d.soff = cpre[k];
+    d.meta_src = (int64_t)mstart;
+    d.v_lo = A.vlo;
+    d.meta_bytes = hd.o_rptr;
+    d.o_rptr = hd.o_rptr;
+    d.o_val = hd.o_val;
+    d.o_ridx = hd.o_ridx;
+    d.o_rval = hd.o_rval;
+    d.nv = (int32_t)nv;
+    d.r_lo = (int32_t)A.rlo;
+    d.nrow1 = (int32_t)nrow1;
+    d.e_lo = (int32_t)A.elo;
+    d.nent = (int32_t)nent;
+    pd[k] = d;
+  }
+  // cross-task combine slots (group scratch bases)
+  {
+    int64_t sl = 0;
+    for (int64_t i = 0; i < nit;) {
+      const int64_t np = It[i].np;
+      for (int64_t q = i; q < i + np; ++q) {
+        Xg[q].slot = np > 1 ? sl : 0;
+        Xg[q].g = It[q].g;
+        Xg[q].p = It[q].p;
+        Xg[q].npieces = (int32_t)np;
+      }
+      if (np > 1) sl += np * kGroupRows;
+      i += np;
+    }
   }
 
+  // ---- upload and pack
   h->n_groups = ngroups;
   h->n_items = nit;
   h->n_chunks = nch;
   h->n_runs = nrun;
-  h->chunks = dev_alloc<Chunk>(nch, st);
-  if (nch) SB_CU(cudaMemcpyAsync(h->chunks, Ch.data(), sizeof(Chunk) * nch, cudaMemcpyHostToDevice, st));
-  h->items = dev_alloc<Item>(nit, st);
+  h->stream_bytes = cpre[nch];
+  h->stream = dev_alloc<unsigned char>(cpre[nch], st);
+  h->cref = dev_alloc<ChunkRef>(nch, st);
   h->xgi = dev_alloc<XgInfo>(nit, st);
   h->task = dev_alloc<int32_t>(ntask + 1, st);
-  if (nit) {
-    SB_CU(cudaMemcpyAsync(h->items, It.data(), sizeof(Item) * nit, cudaMemcpyHostToDevice, st));
-    SB_CU(cudaMemcpyAsync(h->xgi, Xg.data(), sizeof(XgInfo) * nit, cudaMemcpyHostToDevice, st));
+  if (nch) {
+    SB_CU(cudaMemcpyAsync(h->cref, cref.data(), sizeof(ChunkRef) * nch, cudaMemcpyHostToDevice, st));
+    DevBuf mb, pb;
+    SB_CU(mb.alloc(meta.size(), st));
+    SB_CU(pb.alloc(sizeof(PackDesc) * nch, st));
+    SB_CU(cudaMemcpyAsync(mb.p, meta.data(), meta.size(), cudaMemcpyHostToDevice, st));
+    SB_CU(cudaMemcpyAsync(pb.p, pd.data(), sizeof(PackDesc) * nch, cudaMemcpyHostToDevice, st));
+    k_pack_stream<T><<<(unsigned)nch, 256, 0, st>>>(pb.as<PackDesc>(), mb.as<unsigned char>(),
+                                                    h->rem_ptr, static_cast<const T*>(h->tval),
+                                                    h->rem_idx, static_cast<const T*>(h->rem_val),
+                                                    h->stream);
+    SB_CU(cudaGetLastError());
+    SB_CU(cudaStreamSynchronize(st));
   }
+  if (nit)
+    SB_CU(cudaMemcpyAsync(h->xgi, Xg.data(), sizeof(XgInfo) * nit, cudaMemcpyHostToDevice, st));
   SB_CU(cudaMemcpyAsync(h->task, task.data(), sizeof(int32_t) * (ntask + 1), cudaMemcpyHostToDevice, st));
   h->scratch_elems = slot;
   h->scratch = dev_alloc<T>(slot, st);
   h->counters = dev_alloc<int32_t>(ngroups, st);
   SB_CU(cudaMemsetAsync(h->counters, 0, sizeof(int32_t) * std::max<int64_t>(ngroups, 1), st));
-  SB_CU(cudaStreamSynchronize(st));  // It / Xg / R / Ch / task are host temporaries
+  SB_CU(cudaStreamSynchronize(st));  // host temporaries
   cudaFree(h->xt);  // the per-tile map was only needed to plan
   h->xt = nullptr;
+}
+
+// The remainder executor's plan: packets of whole consecutive rows with up to
+// kPacketEntries entries and kPacketRows rows (every local row is in one, so
+// the executor writes every row); a row longer than kPieceLen is cut into
+// warp pieces of kPieceLen entries, summed in order by the last to arrive.
+template <typename T>
+void plan_remainder(sable_handle* h, const std::vector<int32_t>& H_rp, cudaStream_t st) {
+  const int64_t nloc = (int64_t)H_rp.size() - 1;
+  std::vector<RemPacket> pk;
+  int64_t slot = 0, nlong = 0;
+  int64_t r = 0;
+  while (r < nloc) {
+    const int64_t len = (int64_t)H_rp[r + 1] - H_rp[r];
+    if (len > kPieceLen) {
+      const int32_t np = (int32_t)((len + kPieceLen - 1) / kPieceLen);
+      for (int32_t q = 0; q < np; ++q) {
+        RemPacket p{};
+        p.r0 = (int32_t)r;
+        p.r1 = -1 - q;
+        p.e0 = (int32_t)(H_rp[r] + (int64_t)q * kPieceLen);
+        p.e1 = (int32_t)std::min<int64_t>(H_rp[r + 1], (int64_t)p.e0 + kPieceLen);
+        p.npieces = np;
+        p.slot = (int32_t)slot;
+        p.counter = (int32_t)nlong;
+        pk.push_back(p);
+      }
+      slot += np;
+      ++nlong;
+      ++r;
+      continue;
+    }
+    RemPacket p{};
+    p.r0 = (int32_t)r;
+    p.e0 = H_rp[r];
+    int64_t r1 = r;
+    while (r1 < nloc && r1 - r < kPacketRows) {
+      const int64_t l1 = (int64_t)H_rp[r1 + 1] - H_rp[r1];
+      if (l1 > kPieceLen) break;
+      if (r1 > r && (int64_t)H_rp[r1 + 1] - H_rp[r] > kPacketEntries) break;
+      ++r1;
+    }
+    p.r1 = (int32_t)r1;
+    p.e1 = H_rp[r1];
+    pk.push_back(p);
+    r = r1;
+  }
+  RemHost& R = h->rp;
+  R.n_packets = (int64_t)pk.size();
+  R.n_pieces = slot;
+  R.n_long = nlong;
+  R.packets = dev_alloc<RemPacket>(R.n_packets, st);
+  R.scratch = dev_alloc<T>(slot, st);
+  R.counters = dev_alloc<int32_t>(nlong, st);
+  SB_CU(cudaMemsetAsync(R.counters, 0, sizeof(int32_t) * std::max<int64_t>(nlong, 1), st));
+  if (R.n_packets)
+    SB_CU(cudaMemcpyAsync(R.packets, pk.data(), sizeof(RemPacket) * pk.size(), cudaMemcpyHostToDevice, st));
+  SB_CU(cudaStreamSynchronize(st));
 }
 
 // ------------------------------------------------------------------- inspect
@@ -1226,6 +1459,7 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
   ExecCfg cfg = exec_config((int)sv);
   plan_executor<T>(h, cfg, nbl, b0, H_rpntr, H_W, br_vbase, br_wprefix, H_rp, H_xt, st);
   h->cfg = cfg;
+  plan_remainder<T>(h, H_rp, st);
 
   // ---- bookkeeping ---------------------------------------------------------------------
   int64_t nnz = 0;
@@ -1236,13 +1470,11 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
     for (int64_t c : cc) nnz += c;
   }
   h->nnz = nnz;
-  // algorithmic bytes per SpMV: tile values + item and
-  // chunk descriptors + remainder (value, index) + row
+  // algorithmic bytes per SpMV: tile
+  // values + a 12-byte descriptor per tile + remainder (value, index) + row
   // pointers + x read once + y written once
-  h->bytes_alg = tile_elems * (int64_t)sv + h->n_items * (int64_t)sizeof(Item) +
-                 h->n_chunks * (int64_t)sizeof(Chunk) +
-                 n_rem * (int64_t)(sv + 4) + (nloc + 1) * 4 + ncols * (int64_t)sv +
-                 nloc * (int64_t)sv;
+  h->bytes_alg = tile_elems * (int64_t)sv + n_dense * 12 + n_rem * (int64_t)(sv + 4) +
+                 (nloc + 1) * 4 + ncols * (int64_t)sv + nloc * (int64_t)sv;
   SB_CU(cudaStreamSynchronize(st));
 }
 

@@ -8,9 +8,10 @@
 //            nr x W_a slab is stored column-major (leading dimension nr), the
 //            groups of a block row back to back.  For h <= 32 this is exactly
 //            the paper's column-major tile storage.
-//   items  : one 32-byte Item per warp work unit (row group or piece of one),
-//            in row order; xgi: cross-task combine data per item.
-//   chunks : one 64-byte Chunk per stage load (consecutive items).
+//   stream : the executor's input, chunk after chunk; each chunk (<= one
+//            stage) = header, item descriptors, bundle lane maps, x gather
+//            segments, its rows' remainder pointers, its dense values, its
+//            remainder columns and values -- copied with one bulk copy.
 //   task   : per executor warp, a contiguous chunk range of about equal bytes.
 //   tiles  : export geometry of the dense tiles (TileDesc).
 //   rem_*  : the CSR remainder of the local rows (int32 row pointers).
@@ -26,8 +27,8 @@
 namespace sable {
 
 constexpr int kGroupRows = 32;  // rows per row group (= warp width)
-constexpr int kRE = 256;        // remainder entries per item (per-warp product buffer)
 constexpr int kWarps = 4;       // warps per executor CTA
+constexpr int kMaxStages = 4;   // per-warp stage ring
 
 struct TileDesc {  // export geometry of a dense tile
   int32_t c0;  // first global column of the tile
@@ -51,62 +52,77 @@ enum : uint8_t {
   IF_XG = 4,     // the group's pieces are in several warp tasks (global combine)
 };
 
-// One unit of a warp's stream (32 B): a whole row group, or a piece of a
-// split group -- a range of panel columns inside one run, or a range of the
-// group's remainder entries.  Items never span runs, so the x of item
-// column c is x[xo + c].
-struct Item {
-  int64_t voff;   // first dense value (group slab column-major, ld nr)
-  int32_t eb;     // first remainder entry (position in the local CSR)
-  int32_t xo;     // x index of the item's first dense column
-  int32_t row0;   // first local row of the group
-  int16_t ncol;   // dense columns of the item (0 = remainder only)
-  int16_t ne;     // remainder entries [eb, eb + ne), <= kRE
-  uint16_t qm;    // floor(32768 / nr) + 1: lane / nr == (lane * qm) >> 15 for lane < 32
-  int16_t xb;     // first element of the item's dense x in its chunk's x buffer
-  uint8_t nr;     // rows (1..32)
-  uint8_t q;      // column phases 32 / nr
-  uint8_t flags;  // IF_*
-  uint8_t pad_;
+// Where a chunk's stream lives (16 B).
+struct ChunkRef {
+  int64_t off;    // byte offset in the stream buffer (128-aligned)
+  int32_t bytes;  // stream bytes (multiple of 16; 0 = no chunk)
+  int32_t pad_;
 };
-static_assert(sizeof(Item) == 32, "Item is 32 B");
 
-// Cross-task combine data of an IF_XG item (side table, read only for those).
+// The executor's HBM input is one byte stream, chunk after chunk; a chunk is
+// copied into a warp's stage with ONE bulk copy and describes itself:
+//   [ChunkHdr | items | lane maps | x gathers | rem_ptr | values | rem cols | rem vals]
+// every region 16-byte aligned, offsets relative to the chunk start.
+struct ChunkHdr {
+  ChunkRef next;   // the chunk nstage ahead in the same warp task (bytes 0: none)
+  uint16_t o_item, o_lane, o_gath, o_rptr, o_val, o_ridx, o_rval;
+  uint16_t ni;     // items
+  uint16_t nb;     // bundles (32 lane maps each)
+  uint16_t ng;     // x gather segments
+  uint16_t ndx;    // dense x elements; the chunk's x buffer is [dense x | remainder x]
+  uint16_t pad16_;
+  int32_t r0;      // local row whose pointer is rem_ptr element 0 of the chunk
+  int32_t e0;      // first remainder entry (rem_ptr values are relative to it after -e0)
+  int32_t nent;    // remainder entries
+  int32_t i0;      // global index of the chunk's first item
+  int32_t pad_[2];
+};
+static_assert(sizeof(ChunkHdr) == 64, "ChunkHdr is 64 B");
+
+// One work item in a chunk (16 B): a whole row group (nr <= 32 rows of one
+// block row: its dense slab, column-major with leading dimension nr, and its
+// remainder entries), or a piece of a group larger than a stage.
+struct SItem {
+  uint16_t v;      // element offset of the slab in the chunk's value region
+  uint16_t e;      // element offset of the entries in the chunk's entry regions
+  uint16_t ne;     // remainder entries
+  uint16_t ncol;   // dense columns; their x is xbuf[xb .. xb + ncol)
+  int32_t row0;    // first local row of the group
+  uint16_t xb;     // dense x offset in the chunk's x buffer
+  uint8_t nr;      // rows (1..32)
+  uint8_t flags;   // IF_*
+};
+static_assert(sizeof(SItem) == 16, "SItem is 16 B");
+
+// A bundle maps the 32 lanes of a warp onto the rows of several consecutive
+// items: lane = base_i + ph * nr_i + r works on row r of item i, columns and
+// entries ph, ph + Q_i, ... (Q_i = 2^lq phases, chosen by the planner to even
+// out the lanes' work).  Packed lane map (4 B):
+//   item (8 b) | row (5 b) << 8 | ph (5 b) << 13 | lq (3 b) << 18 | valid << 21
+constexpr uint32_t kLaneValid = 1u << 21;
+
+// One dense x segment of a chunk: xbuf[dst + i] = x[xs + i] for i < n.
+struct Gather {
+  int32_t xs;
+  uint16_t n;
+  uint16_t dst;
+};
+static_assert(sizeof(Gather) == 8, "Gather is 8 B");
+
+// Cross-task combine data of an IF_XG item (side table by global item index).
 struct XgInfo {
   int64_t slot;     // scratch base (npieces * 32 partials)
   int32_t g;        // arrival counter index
-  int16_t p;        // piece index
-  int16_t pad_;
+  int32_t p;        // piece index
   int32_t npieces;  // pieces of the group
-  int32_t pad2_;
+  int32_t pad_;
 };
 static_assert(sizeof(XgInfo) == 24, "XgInfo is 24 B");
-
-// Streamed arrays of a chunk, in stage order.
-enum { SR_ITEM = 0, SR_RPTR, SR_VAL, SR_RIDX, SR_RVAL, SR_N };
-
-// One stage load of a warp (64 B): consecutive items whose data are
-// contiguous ranges of five arrays, copied with 1-D bulk copies (16-byte
-// granular) into the warp's stage after a 64-byte slot that carries the
-// descriptor of the chunk nstage ahead.  Offsets are precomputed by the
-// planner, so issuing a chunk is five copy instructions.
-struct Chunk {
-  uint32_t src16[SR_N];  // first byte / 16 of each range in its array
-  uint16_t bytes[SR_N];  // bytes copied (multiple of 16; 0 = none)
-  uint16_t off[SR_N];    // stage offset of the first wanted element (dst = off & ~15)
-  int64_t v0;            // dense value index of the chunk's first value
-  int32_t e0;            // remainder entry of the chunk's first entry
-  int32_t r0;            // local row whose pointer is rem_ptr element 0 of the stage
-  int16_t ni;            // items
-  int16_t ndx;           // dense x elements; the x buffer is [dense x | remainder x]
-  int32_t i0;            // index of the chunk's first item
-};
-static_assert(sizeof(Chunk) == 64, "Chunk is 64 B");
 
 // Executor shape (runtime; the planner sizes items, chunks and tasks for it).
 struct ExecCfg {
   int32_t item_bytes;   // cap on one item's streamed bytes
-  int32_t stage_bytes;  // bytes of one stage (per warp), multiple of 128
+  int32_t stage_bytes;  // bytes of one stage (per warp), multiple of 128, <= 65536
   int32_t nstage;       // stages in each warp's ring (2..4)
   int32_t xbuf;         // x elements gathered per chunk (dense columns + remainder entries)
   int32_t ctas_per_sm;  // CTAs (kWarps warps each) per SM
@@ -114,31 +130,60 @@ struct ExecCfg {
   int32_t mode;         // diagnostics: 0 = full; 1 = stream only
 };
 
-constexpr int kMaxStages = 4;
-
-// Shared memory of one warp: mbarriers + chunk descriptors (512 B), two x
-// buffers [xbuf] (the chunk being computed, the next one being gathered),
-// then the stages.
+// Shared memory of one warp: mbarriers + chunk refs (256 B), two x buffers
+// [xbuf] (the chunk being computed, the next one being gathered), the stages.
 inline __host__ __device__ uint32_t warp_smem_bytes(int nstage, int stage_bytes, int xbuf, int sv) {
-  return 512 + (uint32_t)((2 * xbuf * sv + 127) & ~127) + (uint32_t)(nstage * stage_bytes);
+  return 256 + (uint32_t)((2 * xbuf * sv + 127) & ~127) + (uint32_t)(nstage * stage_bytes);
 }
 
 // Device-side view used by the executor kernel.
 template <typename T>
 struct Plan {
-  const Chunk* chunks;
-  const int32_t* task;  // n_tasks + 1 chunk boundaries
-  const Item* items;
+  const unsigned char* stream;
+  const ChunkRef* cref;   // per chunk (the prologue of each task)
+  const int32_t* task;    // n_tasks + 1 chunk boundaries
   const XgInfo* xgi;
-  const T* tval;
-  const int32_t* rem_ptr;  // local rows + 1
-  const int32_t* rem_idx;
-  const T* rem_val;
   T* scratch;
   int32_t* counters;
   int32_t n_tasks;
   int32_t nstage, stage_bytes, xbuf;
   int32_t mode;
+};
+
+// ---- CSR remainder executor (rem.cu)
+
+constexpr int kPieceLen = 512;   // remainder rows longer than this are cut into warp pieces (<= kPacketEntries)
+constexpr int kPacketEntries = 512;  // entries per row-range packet (whole rows)
+constexpr int kPacketRows = 256;     // rows per row-range packet
+
+// One warp's work in the remainder executor (32 B): a range of whole rows
+// [r0, r1) and their entries [e0, e1), or one piece of a long row.
+struct RemPacket {
+  int32_t r0, r1;    // rows (piece: r0 = its row, r1 = -1 - piece index)
+  int32_t e0, e1;    // entries
+  int32_t npieces;   // piece: pieces of its row
+  int32_t slot;      // piece: scratch base of its row's partials
+  int32_t counter;   // piece: arrival counter of its row
+  int32_t pad_;
+};
+static_assert(sizeof(RemPacket) == 32, "RemPacket is 32 B");
+
+template <typename T>
+struct RemPlan {
+  const RemPacket* packets;
+  const int32_t* ptr;  // local CSR row pointers
+  const int32_t* idx;
+  const T* val;
+  T* scratch;
+  int32_t* counters;
+  int64_t n_packets;
+};
+
+struct RemHost {
+  RemPacket* packets = nullptr;
+  void* scratch = nullptr;
+  int32_t* counters = nullptr;
+  int64_t n_packets = 0, n_pieces = 0, n_long = 0;
 };
 
 // Internal position of element (r, c) of a tile whose first panel column is
@@ -173,11 +218,13 @@ struct sable_handle {
   int64_t n_dense = 0;
   sable::XTile* xt = nullptr;        // per tile (plan time only, freed after)
   int64_t n_runs = 0;
-  sable::Item* items = nullptr;
+  unsigned char* stream = nullptr;   // executor byte stream (chunk after chunk)
+  int64_t stream_bytes = 0;
+  sable::ChunkRef* cref = nullptr;   // per chunk
   sable::XgInfo* xgi = nullptr;      // per item
-  sable::Chunk* chunks = nullptr;
   int32_t* task = nullptr;           // warp task chunk boundaries (n_tasks + 1)
   int64_t n_groups = 0, n_items = 0, n_chunks = 0;
+  sable::RemHost rp;                 // remainder executor plan
   sable::ExecCfg cfg{};
   int32_t* rem_ptr = nullptr;
   int32_t* rem_idx = nullptr;

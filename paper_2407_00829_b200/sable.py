@@ -62,7 +62,8 @@ class sable_info(C.Structure):
                 ("n_groups", C.c_int64), ("n_items", C.c_int64),
                 ("dtype", C.c_int32), ("delta", C.c_int32), ("suitable", C.c_int32),
                 ("world", C.c_int32), ("rank", C.c_int32), ("inspect_ms", C.c_double),
-                ("n_tasks", C.c_int64), ("exec_grid", C.c_int32), ("item_bytes", C.c_int32)]
+                ("n_tasks", C.c_int64), ("exec_grid", C.c_int32), ("item_bytes", C.c_int32),
+                ("rem_packets", C.c_int64), ("rem_long_pieces", C.c_int64)]
 
 
 class sable_partition_host(C.Structure):
