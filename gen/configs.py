@@ -400,15 +400,42 @@ def make_c5(seed: int = 5, scale: float = 1.0) -> Synth:
     rows = np.repeat(np.arange(n, dtype=np.int64), deg)
     keys = rows * n + gs.integers(0, n, size=len(rows), dtype=np.int64)
     keys = np.unique(keys)
-    # top up rows that lost columns to in-row collisions (distinct columns)
-    for _ in range(100):
-        have = np.bincount(keys // n, minlength=n)
-        short = np.flatnonzero(have < deg)
-        if len(short) == 0:
-            break
-        r = np.repeat(short, deg[short] - have[short])
-        extra = r * n + gs.integers(0, n, size=len(r), dtype=np.int64)
-        keys = np.unique(np.concatenate([keys, extra]))
+    # top up the rows that lost columns to in-row collisions (distinct
+    # columns): heavy rows (deg > n / 8) are drawn without replacement, the
+    # others are redrawn with oversampling until every row has its degree
+    have = np.bincount(keys // n, minlength=n)
+    short = np.flatnonzero(have < deg)
+    if len(short):
+        is_short = np.zeros(n, dtype=bool)
+        is_short[short] = True
+        sel = is_short[keys // n]
+        sk, keys = keys[sel], keys[~sel]
+        heavy = short[deg[short] > n // 8]
+        light = short[deg[short] <= n // 8]
+        hk = [r * n + np.sort(gs.choice(n, size=int(deg[r]), replace=False)) for r in heavy.tolist()]
+        sk = sk[~np.isin(sk // n, heavy)]
+        for _ in range(1000):
+            need = deg[light] - np.bincount(sk // n, minlength=n)[light]
+            todo = need > 0
+            if not todo.any():
+                break
+            r = np.repeat(light[todo], 2 * need[todo] + 4)
+            new = r * n + gs.integers(0, n, size=len(r), dtype=np.int64)
+            # keep every old key and, per row, the first new distinct keys in
+            # draw order (not value order) up to the row's degree
+            new, first_pos = np.unique(new, return_index=True)
+            new_keep = ~np.isin(new, sk, assume_unique=True)
+            new, first_pos = new[new_keep], first_pos[new_keep]
+            order = np.argsort(first_pos, kind="stable")  # draw order
+            new = new[order]
+            nr_ = new // n
+            o2 = np.argsort(nr_, kind="stable")  # group by row, draw order within
+            new, nr_ = new[o2], nr_[o2]
+            start = np.searchsorted(nr_, nr_, side="left")
+            rank = np.arange(len(new)) - start
+            have_r = np.bincount(sk // n, minlength=n)
+            sk = np.sort(np.concatenate([sk, new[rank < (deg[nr_] - have_r[nr_])]]))
+        keys = np.sort(np.concatenate([keys, sk] + hk))
     rem_nnz = len(keys)
     target = 0.4 / 0.6 * rem_nnz
     occ = _Occupancy(256)
