@@ -334,9 +334,11 @@ cudaError_t launch_rem(const sable_handle* h, const void* x, void* y, cudaStream
 // sum, or 0), then the dense-tile executor adds the dense part of the rows
 // of block rows with tiles.
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st) {
-  cudaError_t e = h->dtype == SABLE_F64 ? launch_rem<double>(h, x, y, st)
-                                        : launch_rem<float>(h, x, y, st);
-  if (e != cudaSuccess) return e;
+  // diagnostics (SABLE_EXEC_MODE): 2 = remainder executor only, 3 = dense only
+  cudaError_t e = cudaSuccess;
+  if (h->cfg.mode != 3)
+    e = h->dtype == SABLE_F64 ? launch_rem<double>(h, x, y, st) : launch_rem<float>(h, x, y, st);
+  if (e != cudaSuccess || h->cfg.mode == 2) return e;
   return h->dtype == SABLE_F64 ? launch_spmv<double>(h, x, y, st)
                                : launch_spmv<float>(h, x, y, st);
 }

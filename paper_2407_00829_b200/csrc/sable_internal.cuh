@@ -127,7 +127,7 @@ struct ExecCfg {
   int32_t xbuf;         // x elements gathered per chunk (dense columns + remainder entries)
   int32_t ctas_per_sm;  // CTAs (kWarps warps each) per SM
   int32_t n_tasks;      // warp tasks = grid * kWarps
-  int32_t mode;         // diagnostics: 0 = full; 1 = stream only
+  int32_t mode;         // diagnostics: 0 = full; 1 = dense streams only; 2 = remainder only; 3 = dense only
 };
 
 // Shared memory of one warp: mbarriers + chunk refs (256 B), two x buffers
