@@ -21,7 +21,7 @@ for c in $CFGS; do
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
       --log-file $OUT/launches_$c.csv python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline \
       > $OUT/ncu_launch_$c.log 2>&1; echo "ncu launches $c rc=$?"
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmv -s 3 -c 1 \
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:"spmv|rem_kernel" -s 6 -c 2 \
       -o $OUT/spmv_$c python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline \
       > $OUT/ncu_full_$c.log 2>&1; echo "ncu full $c rc=$?"
   fi

@@ -81,7 +81,8 @@ def main():
                     lines.append(f"- {key}: {k[key][0]} {k[key][1]}")
             rd, wr = num(k, "dram__bytes_read.sum"), num(k, "dram__bytes_write.sum")
             if rd is not None and wr is not None:
-                traffic.setdefault(cfg, int(rd + wr))
+                # one SpMV = the captured launches of one step: sum them
+                traffic[cfg] = traffic.get(cfg, 0) + int(rd + wr)
                 lines.append(f"- traffic (read+write): {int(rd + wr)} B")
             stalls = sorted(((float(v[0]), kk) for kk, v in k.items()
                              if kk.startswith("smsp__pcsamp_warps_issue_stalled_")
@@ -95,12 +96,16 @@ def main():
     for lf in sorted(glob.glob(os.path.join(d, "launches_*.csv"))):
         cfg = re.sub(r"^launches_|\.csv$", "", os.path.basename(lf))
         rows = launch_shares(lf)
-        sp = [t for n, t in rows if "spmv" in n]
+        sp = [t for n, t in rows if "spmv_kernel" in n]
+        rm = [t for n, t in rows if "rem_kernel" in n]
         lines.append(f"## {cfg}: launch list ({len(rows)} launches)")
-        if sp:
-            # the last launches of the run are the timed/kernel-only steps:
-            # one step = one spmv launch (+ the L2 scrub, which is not ours)
-            lines.append(f"- spmv launches: {len(sp)}; median {sorted(sp)[len(sp) // 2] * 1e6:.2f} us")
+        med = lambda v: sorted(v)[len(v) // 2] if v else 0.0  # noqa: E731
+        if sp or rm:
+            # one SpMV step = rem_kernel + spmv_kernel (+ the L2 scrub, not ours)
+            a, b = med(rm), med(sp)
+            lines.append(f"- rem_kernel launches: {len(rm)}, median {a * 1e6:.2f} us; "
+                         f"spmv_kernel launches: {len(sp)}, median {b * 1e6:.2f} us; "
+                         f"dense share of one SpMV: {b / max(a + b, 1e-12):.2f}")
         tot = {}
         for n, t in rows:
             short = n.split("(")[0]
