@@ -14,15 +14,15 @@
 // shared-memory stages, ONE 1-D bulk copy per chunk (cp.async.bulk, L2
 // evict-first, completion on the stage's mbarrier); a chunk's header names
 // the chunk nstage ahead, so no warp ever waits on a descriptor and no warp
-// waits on another.  While chunk k is computed, the x it needs for chunk
-// k + 1 (its dense columns' segments and one x per remainder entry) is
-// copied into the other half of the warp's x buffer with 4/8-byte
-// asynchronous copies (LDGSTS).  Chunk k is computed bundle by bundle: a
+// waits on another.  While chunk k is computed, the x lines chunk k + 1 will
+// read are prefetched into L1 (one prefetch per 128-byte line of each run of
+// consecutive global columns).  Chunk k is computed bundle by bundle: a
 // bundle maps the 32 lanes onto the rows of several items -- lane = (item,
 // row r, phase ph of Q) -- chosen by the planner so that the lanes' work is
 // even; a lane sums columns ph, ph + Q, ... of its row of the column-major
-// slab and entries ph, ph + Q, ... of its row's remainder, all from shared
-// memory; the phases fold with shuffles; the row is written once.  Pieces of
+// slab from shared memory times x read through L1 (x of column c is
+// x[off + c] of the run holding c); the phases fold with shuffles; the row
+// is written once.  Pieces of
 // a group larger than a stage are summed left to right in registers (or, if
 // two tasks share the group, in global scratch by the last piece to arrive).
 // No atomics on y; every row's summation order depends on the matrix alone,
@@ -71,23 +71,6 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// 4- or 8-byte asynchronous global -> shared copy (LDGSTS, through L1).
-template <typename T>
-__device__ __forceinline__ void cp_async(T* dst, const T* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "n"((int)sizeof(T))
-               : "memory");
-}
-
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
                                          uint32_t bar, uint64_t policy) {
   asm volatile(
@@ -121,33 +104,34 @@ __device__ __forceinline__ void issue_chunk(const unsigned char* stream, const C
   bulk_g2s(smem_u32(stage), stream + c.off, (uint32_t)c.bytes, bar, pol);
 }
 
-// Start copying the x a staged chunk needs into an x buffer: the dense
-// segments (contiguous global columns), then one x per remainder entry.
-// Asynchronous (LDGSTS): it overlaps the computation of the previous chunk.
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// Bring the x lines a staged chunk will read into L1 (one prefetch per 128-B
+// line of each x run), while the previous chunk is computed.
 template <typename T>
-__device__ __forceinline__ void gather_chunk(const unsigned char* stage, T* xb,
-                                             const T* __restrict__ x, int lane) {
+__device__ __forceinline__ void prefetch_chunk(const unsigned char* stage,
+                                               const T* __restrict__ x, int lane) {
   const ChunkHdr& H = *reinterpret_cast<const ChunkHdr*>(stage);
-  const Gather* ga = reinterpret_cast<const Gather*>(stage + H.o_gath);
-  for (int g = 0; g < H.ng; ++g) {
-    const Gather G = ga[g];
-    for (int i = lane; i < G.n; i += 32) cp_async(xb + G.dst + i, x + G.xs + i);
+  const XRun* xr = reinterpret_cast<const XRun*>(stage + H.o_gath);
+  constexpr int kLine = 128 / (int)sizeof(T);
+  for (int g = lane; g < H.ng; g += 32) {
+    const XRun R = xr[g];
+    for (int c = R.cbeg; c < R.cend; c += kLine) prefetch_l1(x + R.off + c);
+    prefetch_l1(x + R.off + R.cend - 1);
   }
-  const int32_t* ri = reinterpret_cast<const int32_t*>(stage + H.o_ridx);
-  T* xr = xb + H.ndx;
-  for (int e = lane; e < H.nent; e += 32) cp_async(xr + e, x + ri[e]);
 }
 
 template <typename T>
 __device__ __forceinline__ void compute_chunk(const Plan<T>& P, const unsigned char* stage,
-                                              const T* xb, T* __restrict__ y, T& run, int lane) {
+                                              const T* __restrict__ x, T* __restrict__ y,
+                                              T& run, int lane) {
   const ChunkHdr& H = *reinterpret_cast<const ChunkHdr*>(stage);
   const SItem* items = reinterpret_cast<const SItem*>(stage + H.o_item);
   const uint32_t* lmap = reinterpret_cast<const uint32_t*>(stage + H.o_lane);
-  const int32_t* rptr = reinterpret_cast<const int32_t*>(stage + H.o_rptr);
+  const XRun* runs = reinterpret_cast<const XRun*>(stage + H.o_gath);
   const T* val = reinterpret_cast<const T*>(stage + H.o_val);
-  const T* rval = reinterpret_cast<const T*>(stage + H.o_rval);
-  const T* xr = xb + H.ndx;
   for (int b = 0; b < H.nb; ++b) {
     const uint32_t m = lmap[b * 32 + lane];
     const bool valid = (m & kLaneValid) != 0;
@@ -156,34 +140,41 @@ __device__ __forceinline__ void compute_chunk(const Plan<T>& P, const unsigned c
     if (valid) I = items[m & 255];
     const int nr = I.nr;
     T acc = T(0);
-    if (valid) {
-      // dense: columns ph, ph + Q, ... of row r (column-major slab, ld nr)
+    if (valid && ph < I.ncol) {
+      // columns ph, ph + Q, ... of row r; x of column c is x[off + c] of the
+      // run holding c (runs in column order; two accumulators)
+      int k = I.xb;
+      XRun R = runs[k];
+      while (R.cend <= ph) R = runs[++k];
+      const T* xr = x + R.off;
+      int rend = R.cend;
       const T* vp = val + I.v + ph * nr + r;
-      const T* xs = xb + I.xb;
       const int step = Q * nr;
-      // two interleaved accumulators (columns 2j and 2j + 1 of the lane)
-      // for ILP; the order is fixed by the item alone
       T acc1 = T(0);
       int c = ph;
-      for (; c + 3 * Q < I.ncol; c += 4 * Q) {
-        acc = fma(vp[0], xs[c], acc);
-        acc1 = fma(vp[step], xs[c + Q], acc1);
-        acc = fma(vp[2 * step], xs[c + 2 * Q], acc);
-        acc1 = fma(vp[3 * step], xs[c + 3 * Q], acc1);
-        vp += 4 * step;
-      }
-      for (; c < I.ncol; c += Q) {
-        acc = fma(*vp, xs[c], acc);
-        vp += step;
+      for (;;) {
+        while (c >= rend) {  // the run holding column c
+          R = runs[++k];
+          xr = x + R.off;
+          rend = R.cend;
+        }
+        if (c + 3 * Q < rend) {
+          const T x0 = __ldg(xr + c), x1 = __ldg(xr + c + Q), x2 = __ldg(xr + c + 2 * Q),
+                  x3 = __ldg(xr + c + 3 * Q);
+          acc = fma(vp[0], x0, acc);
+          acc1 = fma(vp[step], x1, acc1);
+          acc = fma(vp[2 * step], x2, acc);
+          acc1 = fma(vp[3 * step], x3, acc1);
+          vp += 4 * step;
+          c += 4 * Q;
+        } else {
+          acc = fma(*vp, __ldg(xr + c), acc);
+          vp += step;
+          c += Q;
+        }
+        if (c >= I.ncol) break;
       }
       acc += acc1;
-      // remainder: entries ph, ph + Q, ... of row r within the item's entries
-      if (I.ne > 0) {
-        const int rr = I.row0 + r - H.r0;
-        const int e_lo = I.e, e_hi = I.e + I.ne;  // chunk-relative
-        const int lo = max(rptr[rr] - H.e0, e_lo), hi = min(rptr[rr + 1] - H.e0, e_hi);
-        for (int e = lo + ph; e < hi; e += Q) acc = fma(rval[e], xr[e], acc);
-      }
     }
     // fold the phases: lane ph * nr + r collects ph + 1, ph + 2, ... in order
     // of a binary tree (fixed by Q and nr: deterministic)
@@ -237,8 +228,7 @@ __global__ void __launch_bounds__(kThreads)
   unsigned char* ws =
       smem + (size_t)warp * warp_smem_bytes(NS, P.stage_bytes, P.xbuf, (int)sizeof(T));
   uint64_t* full = reinterpret_cast<uint64_t*>(ws);  // [kMaxStages]
-  T* xbuf = reinterpret_cast<T*>(ws + 256);          // [2][P.xbuf]
-  unsigned char* stages = ws + 256 + ((2 * P.xbuf * (int)sizeof(T) + 127) & ~127);
+  unsigned char* stages = ws + 256;
 
   uint64_t pol = 0;
   if (lane == 0) {
@@ -251,13 +241,12 @@ __global__ void __launch_bounds__(kThreads)
   }
   __syncwarp();
 
-  // chunk k computes from stage s and x buffer b while chunk k + 1's x is
-  // being gathered into buffer b ^ 1
-  int s = 0, b = 0;
+  // chunk k computes from stage s while chunk k + 1's x lines are being
+  // prefetched into L1
+  int s = 0;
   uint32_t phase = 0;
   mbar_wait(smem_u32(full + 0), 0);
-  if (P.mode != 1) gather_chunk(stages, xbuf, x, lane);
-  cp_async_commit();
+  if (P.mode != 1) prefetch_chunk(stages, x, lane);
   T run = T(0);  // running sum of a split group's pieces (lanes < nr)
   for (int64_t k = kb; k < ke; ++k) {
     int sn = s + 1;
@@ -270,12 +259,9 @@ __global__ void __launch_bounds__(kThreads)
     if (k + 1 < ke) {
       unsigned char* nst = stages + (size_t)sn * P.stage_bytes;
       mbar_wait(smem_u32(full + sn), phn);
-      if (P.mode != 1) gather_chunk(nst, xbuf + (b ^ 1) * P.xbuf, x, lane);
+      if (P.mode != 1) prefetch_chunk(nst, x, lane);
     }
-    cp_async_commit();
-    cp_async_wait<1>();  // chunk k's x
-    __syncwarp();
-    if (P.mode != 1) compute_chunk(P, stage, xbuf + b * P.xbuf, y, run, lane);
+    if (P.mode != 1) compute_chunk(P, stage, x, y, run, lane);
     // refill this stage with the chunk nstage ahead (named by this header)
     __syncwarp();
     if (lane == 0) {
@@ -285,9 +271,7 @@ __global__ void __launch_bounds__(kThreads)
     __syncwarp();
     s = sn;
     phase = phn;
-    b ^= 1;
   }
-  cp_async_wait<0>();
 }
 
 }  // namespace

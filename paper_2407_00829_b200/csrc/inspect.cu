@@ -661,7 +661,7 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
   std::vector<HItem> It;
   It.reserve((size_t)(H_rp.size() / 8 + nbl + 1));
   int64_t slot = 0, ngroups = 0;
-  const int64_t xcap = cfg.xbuf;
+  const int64_t xcap = 32767;  // item columns are 16-bit
   for (int32_t la = 0; la < nbl; ++la) {
     const int32_t a = b0 + la;
     const int32_t hgt = H_rpntr[a + 1] - H_rpntr[a];
@@ -744,8 +744,7 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
   };
   auto fits = [&](const CAcc& A) {
     const int64_t nent = A.de ? A.ehi - A.elo : 0;
-    return chunk_bytes(A) <= cfg.stage_bytes && A.ndx + nent <= xcap && A.ni <= 255 &&
-           nent <= 65535;
+    return chunk_bytes(A) <= cfg.stage_bytes && A.ni <= 255 && nent <= 65535;
   };
   auto add_item = [&](CAcc A, int64_t i) {
     const HItem& it = It[i];
@@ -882,7 +881,7 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
     hd.ni = (uint16_t)A.ni;
     hd.nb = (uint16_t)nb;
     hd.ng = (uint16_t)A.ng;
-    hd.ndx = (uint16_t)A.ndx;
+    hd.ndx = 0;
     hd.r0 = (int32_t)A.rlo;
     hd.e0 = (int32_t)A.elo;
     hd.nent = (int32_t)nent;
@@ -892,8 +891,8 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
     unsigned char* m = meta.data() + mstart;
     memcpy(m, &hd, sizeof(hd));
     SItem* si = reinterpret_cast<SItem*>(m + hd.o_item);
-    Gather* ga = reinterpret_cast<Gather*>(m + hd.o_gath);
-    int64_t xb = 0, gi = 0;
+    XRun* xr = reinterpret_cast<XRun*>(m + hd.o_gath);
+    int64_t gi = 0;
     for (int64_t q = 0; q < A.ni; ++q) {
       const HItem& it = It[A.i0 + q];
       SItem s{};
@@ -902,19 +901,17 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
       s.ne = (uint16_t)it.ne;
       s.ncol = (uint16_t)it.ncol;
       s.row0 = it.row0;
-      s.xb = (uint16_t)xb;
+      s.xb = (uint16_t)gi;
       s.nr = (uint8_t)it.nr;
       s.flags = it.flags;
       si[q] = s;
-      // x gather segments: the runs under the item's columns
+      // x runs: the runs under the item's columns
       for (int64_t c = 0; c < it.ncol;) {
         const int64_t r = run_of(it.xp + c);
         const int64_t end = std::min<int64_t>(it.ncol, (int64_t)R[r + 1].tp - it.xp);
-        ga[gi++] = Gather{(int32_t)(R[r].c0 - R[r].tp + it.xp + c), (uint16_t)(end - c),
-                          (uint16_t)(xb + c)};
+        xr[gi++] = XRun{(int32_t)(R[r].c0 - R[r].tp + it.xp), (uint16_t)c, (uint16_t)end};
         c = end;
       }
-      xb += it.ncol;
     }
     // lane maps
     uint32_t* lm = reinterpret_cast<uint32_t*>(m + hd.o_lane);

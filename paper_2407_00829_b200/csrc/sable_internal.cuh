@@ -68,8 +68,8 @@ struct ChunkHdr {
   uint16_t o_item, o_lane, o_gath, o_rptr, o_val, o_ridx, o_rval;
   uint16_t ni;     // items
   uint16_t nb;     // bundles (32 lane maps each)
-  uint16_t ng;     // x gather segments
-  uint16_t ndx;    // dense x elements; the chunk's x buffer is [dense x | remainder x]
+  uint16_t ng;     // x runs (XRun, o_gath)
+  uint16_t ndx;    // unused (0)
   uint16_t pad16_;
   int32_t r0;      // local row whose pointer is rem_ptr element 0 of the chunk
   int32_t e0;      // first remainder entry (rem_ptr values are relative to it after -e0)
@@ -86,9 +86,9 @@ struct SItem {
   uint16_t v;      // element offset of the slab in the chunk's value region
   uint16_t e;      // element offset of the entries in the chunk's entry regions
   uint16_t ne;     // remainder entries
-  uint16_t ncol;   // dense columns; their x is xbuf[xb .. xb + ncol)
+  uint16_t ncol;   // dense columns
   int32_t row0;    // first local row of the group
-  uint16_t xb;     // dense x offset in the chunk's x buffer
+  uint16_t xb;     // index of the item's first x run in the chunk's run array
   uint8_t nr;      // rows (1..32)
   uint8_t flags;   // IF_*
 };
@@ -101,13 +101,14 @@ static_assert(sizeof(SItem) == 16, "SItem is 16 B");
 //   item (8 b) | row (5 b) << 8 | ph (5 b) << 13 | lq (3 b) << 18 | valid << 21
 constexpr uint32_t kLaneValid = 1u << 21;
 
-// One dense x segment of a chunk: xbuf[dst + i] = x[xs + i] for i < n.
-struct Gather {
-  int32_t xs;
-  uint16_t n;
-  uint16_t dst;
+// One run of an item's columns over consecutive global columns: item columns
+// c in [cbeg, cend) read x[off + c].  An item's runs are consecutive in the
+// chunk's run array and cover its columns in order.
+struct XRun {
+  int32_t off;
+  uint16_t cbeg, cend;
 };
-static_assert(sizeof(Gather) == 8, "Gather is 8 B");
+static_assert(sizeof(XRun) == 8, "XRun is 8 B");
 
 // Cross-task combine data of an IF_XG item (side table by global item index).
 struct XgInfo {
@@ -130,10 +131,11 @@ struct ExecCfg {
   int32_t mode;         // diagnostics: 0 = full; 1 = dense streams only; 2 = remainder only; 3 = dense only
 };
 
-// Shared memory of one warp: mbarriers + chunk refs (256 B), two x buffers
-// [xbuf] (the chunk being computed, the next one being gathered), the stages.
+// Shared memory of one warp: mbarriers (256 B) and the stages.
 inline __host__ __device__ uint32_t warp_smem_bytes(int nstage, int stage_bytes, int xbuf, int sv) {
-  return 256 + (uint32_t)((2 * xbuf * sv + 127) & ~127) + (uint32_t)(nstage * stage_bytes);
+  (void)xbuf;
+  (void)sv;
+  return 256 + (uint32_t)(nstage * stage_bytes);
 }
 
 // Device-side view used by the executor kernel.
