@@ -120,9 +120,27 @@ class ClockSampler:
 
 
 def make_input(config: str):
+    """The seeded synthetic matrix of a config and its VBR input split.  With
+    SABLE_GEN_CACHE=<dir> the generated matrix is saved there once and reused
+    by later runs of the same gpurun call (C5 takes minutes to generate);
+    nothing depends on the cache surviving between calls."""
     import gen
     t = time.time()
-    s = gen.make(config)
+    cache = os.environ.get("SABLE_GEN_CACHE")
+    path = os.path.join(cache, f"{config}.npz") if cache else None
+    if path and os.path.exists(path):
+        z = np.load(path, allow_pickle=False)
+        s = gen.Synth(name=config, nrows=int(z["nrows"]), ncols=int(z["ncols"]),
+                      dtype=z["V"].dtype.type, delta=int(z["delta"]), rpntr=z["rpntr"],
+                      cpntr=z["cpntr"], rects=z["rects"], I=z["I"], J=z["J"], V=z["V"], x=z["x"],
+                      in_rect=z["in_rect"], iterations=int(z["iterations"]))
+    else:
+        s = gen.make(config)
+        if path:
+            os.makedirs(cache, exist_ok=True)
+            np.savez(path, nrows=s.nrows, ncols=s.ncols, delta=s.delta, rpntr=s.rpntr,
+                     cpntr=s.cpntr, rects=s.rects, I=s.I, J=s.J, V=s.V, x=s.x, in_rect=s.in_rect,
+                     iterations=s.iterations)
     inp = s.vbr_input("rect")
     return s, inp, time.time() - t
 
