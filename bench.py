@@ -184,6 +184,14 @@ def run_sable(args):
     xn = torch.empty_like(x)
     flush_l2 = args.config != "c5"  # C5's 1.6 GB working set exceeds L2
     scrub = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    scrub_sink = torch.empty((), dtype=torch.float32, device=dev)
+
+    def flush():
+        # write 512 MiB (> 4x the 126 MB L2), then read it back, so L2 holds
+        # only clean lines of the scrub buffer: none of the SpMV's data, and no
+        # dirty write-back of the scrub's own lines inside the timed region
+        scrub.zero_()
+        torch.sum(scrub, out=scrub_sink)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
 
@@ -198,7 +206,7 @@ def run_sable(args):
               for _ in range(k)]
         for i in range(k):
             if flush_l2:
-                scrub.zero_()
+                flush()
             ev[i][0].record(stream)
             fn()
             ev[i][1].record(stream)
@@ -206,7 +214,7 @@ def run_sable(args):
 
     for _ in range(args.warmup):
         if flush_l2:
-            scrub.zero_()
+            flush()
         step()
     torch.cuda.synchronize()
     if world > 1:
@@ -275,8 +283,11 @@ def run_sable(args):
                 "n_cells": info["n_cells"], "n_dense_tiles": info["n_dense"],
                 "tile_elems": info["tile_elems"], "rem_nnz": info["rem_nnz"],
                 "work_items": info["n_items"], "n_tasks": info["n_tasks"],
+                "n_chunks": info["n_chunks"], "n_bundles": info["n_bundles"],
+                "bundle_lane_fill": round(info["n_bundle_lanes"] / max(1, 32 * info["n_bundles"]), 3),
+                "stream_bytes": info["stream_bytes"], "rem_packets": info["rem_packets"],
                 "exec_grid": info["exec_grid"], "item_bytes": info["item_bytes"],
-                "l2": ("flushed between timed steps (512 MiB write)" if flush_l2 else
+                "l2": ("flushed between timed steps (512 MiB write, then read)" if flush_l2 else
                        "not flushed: working set > L2 (iterated SpMV, cache behaviour is real)"),
                 "parallelism": f"row-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
                 "bytes_alg_per_step": info["bytes_alg"] if world == 1 else None,

@@ -138,6 +138,10 @@ typedef struct {
   int32_t item_bytes;         /* cap on the bytes one work item streams       */
   int64_t rem_packets;        /* remainder executor warps (row packets)       */
   int64_t rem_long_pieces;    /* pieces of remainder rows cut across warps    */
+  int64_t n_chunks;           /* dense executor stage loads (chunks)          */
+  int64_t n_bundles;          /* dense executor lane maps (bundles)           */
+  int64_t stream_bytes;       /* bytes of the dense executor stream           */
+  int64_t n_bundle_lanes;     /* lanes with work summed over the bundles      */
 } sable_info;
 
 /* Caller-allocated HOST buffers for sable_export_partition, sized from

@@ -239,6 +239,10 @@ sable_status sable_get_info(const sable_handle* h, sable_info* info) {
   info->item_bytes = h->cfg.item_bytes;
   info->rem_packets = h->rp.n_packets;
   info->rem_long_pieces = h->rp.n_pieces;
+  info->n_chunks = h->n_chunks;
+  info->n_bundles = h->n_bundles;
+  info->stream_bytes = h->stream_bytes;
+  info->n_bundle_lanes = h->n_bundle_lanes;
   return SABLE_OK;
 }
 

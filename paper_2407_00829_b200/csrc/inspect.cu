@@ -964,6 +964,13 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
   h->n_items = nit;
   h->n_chunks = nch;
   h->n_runs = nrun;
+  h->n_bundles = 0;
+  h->n_bundle_lanes = 0;
+  for (const auto& c : Ch) {
+    h->n_bundles += (int64_t)c.B.size();
+    for (const auto& b : c.B)
+      for (size_t q = 0; q < b.nr.size(); ++q) h->n_bundle_lanes += (int64_t)b.nr[q] << b.lq[q];
+  }
   h->stream_bytes = cpre[nch];
   h->stream = dev_alloc<unsigned char>(cpre[nch], st);
   h->cref = dev_alloc<ChunkRef>(nch, st);

@@ -225,7 +225,7 @@ struct sable_handle {
   sable::ChunkRef* cref = nullptr;   // per chunk
   sable::XgInfo* xgi = nullptr;      // per item
   int32_t* task = nullptr;           // warp task chunk boundaries (n_tasks + 1)
-  int64_t n_groups = 0, n_items = 0, n_chunks = 0;
+  int64_t n_groups = 0, n_items = 0, n_chunks = 0, n_bundles = 0, n_bundle_lanes = 0;
   sable::RemHost rp;                 // remainder executor plan
   sable::ExecCfg cfg{};
   int32_t* rem_ptr = nullptr;

@@ -63,7 +63,9 @@ class sable_info(C.Structure):
                 ("dtype", C.c_int32), ("delta", C.c_int32), ("suitable", C.c_int32),
                 ("world", C.c_int32), ("rank", C.c_int32), ("inspect_ms", C.c_double),
                 ("n_tasks", C.c_int64), ("exec_grid", C.c_int32), ("item_bytes", C.c_int32),
-                ("rem_packets", C.c_int64), ("rem_long_pieces", C.c_int64)]
+                ("rem_packets", C.c_int64), ("rem_long_pieces", C.c_int64),
+                ("n_chunks", C.c_int64), ("n_bundles", C.c_int64), ("stream_bytes", C.c_int64),
+                ("n_bundle_lanes", C.c_int64)]
 
 
 class sable_partition_host(C.Structure):

@@ -9,6 +9,6 @@ for S in "${ARR[@]}"; do
   echo "== $CFG $S" >> $OUT/sw.err; env $S timeout 600 python bench.py --config $CFG --steps 30 --warmup 5 --no-cpu-baseline > $OUT/sw.json 2>> $OUT/sw.err
   python -c "
 import json,sys; d=json.load(open('$OUT/sw.json')); r=d['roofline']
-print('$CFG', '$S'.ljust(70), 'kernel_ms=%.4f frac=%.3f items=%s tasks=%s' % (r['kernel_ms'], r['frac'], d['config']['work_items'], d['config'].get('n_tasks')))
+print('$CFG', '$S'.ljust(70), 'kernel_ms=%.4f frac=%.3f items=%s tasks=%s chunks=%s bundles=%s fill=%s' % (r['kernel_ms'], r['frac'], d['config']['work_items'], d['config'].get('n_tasks'), d['config'].get('n_chunks'), d['config'].get('n_bundles'), d['config'].get('bundle_lane_fill')))
 " 2>&1 | tail -1 | tee -a $OUT/sweep.txt
 done
