@@ -191,7 +191,7 @@ def run_sable(args):
         # only clean lines of the scrub buffer: none of the SpMV's data, and no
         # dirty write-back of the scrub's own lines inside the timed region
         scrub.zero_()
-        torch.sum(scrub, out=scrub_sink)
+        torch.sum(scrub, dim=0, out=scrub_sink)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
 

@@ -118,8 +118,10 @@ __device__ __forceinline__ void prefetch_chunk(const unsigned char* stage,
   constexpr int kLine = 128 / (int)sizeof(T);
   for (int g = lane; g < H.ng; g += 32) {
     const XRun R = xr[g];
-    for (int c = R.cbeg; c < R.cend; c += kLine) prefetch_l1(x + R.off + c);
-    prefetch_l1(x + R.off + R.cend - 1);
+    const T* p = x + R.off;
+    prefetch_l1(p + R.cbeg);
+    for (int c = R.cbeg + kLine; c < R.cend; c += kLine) prefetch_l1(p + c);
+    prefetch_l1(p + R.cend - 1);
   }
 }
 
@@ -141,38 +143,37 @@ __device__ __forceinline__ void compute_chunk(const Plan<T>& P, const unsigned c
     const int nr = I.nr;
     T acc = T(0);
     if (valid && ph < I.ncol) {
-      // columns ph, ph + Q, ... of row r; x of column c is x[off + c] of the
-      // run holding c (runs in column order; two accumulators)
+      // columns ph, ph + Q, ... of row r, run by run (x of column c is
+      // x[off + c] in the run holding c); two accumulators
       int k = I.xb;
       XRun R = runs[k];
       while (R.cend <= ph) R = runs[++k];
-      const T* xr = x + R.off;
-      int rend = R.cend;
       const T* vp = val + I.v + ph * nr + r;
       const int step = Q * nr;
       T acc1 = T(0);
       int c = ph;
       for (;;) {
-        while (c >= rend) {  // the run holding column c
-          R = runs[++k];
-          xr = x + R.off;
-          rend = R.cend;
-        }
-        if (c + 3 * Q < rend) {
-          const T x0 = __ldg(xr + c), x1 = __ldg(xr + c + Q), x2 = __ldg(xr + c + 2 * Q),
-                  x3 = __ldg(xr + c + 3 * Q);
+        const T* xp = x + R.off + c;
+        const int n = (R.cend - c + Q - 1) >> lq;  // this lane's columns in the run
+        int i = 0;
+        for (; i + 3 < n; i += 4) {
+          const T x0 = __ldg(xp), x1 = __ldg(xp + Q), x2 = __ldg(xp + 2 * Q), x3 = __ldg(xp + 3 * Q);
           acc = fma(vp[0], x0, acc);
           acc1 = fma(vp[step], x1, acc1);
           acc = fma(vp[2 * step], x2, acc);
           acc1 = fma(vp[3 * step], x3, acc1);
           vp += 4 * step;
-          c += 4 * Q;
-        } else {
-          acc = fma(*vp, __ldg(xr + c), acc);
-          vp += step;
-          c += Q;
+          xp += 4 * Q;
         }
+        for (; i < n; ++i) {
+          acc = fma(*vp, __ldg(xp), acc);
+          vp += step;
+          xp += Q;
+        }
+        c += n << lq;
         if (c >= I.ncol) break;
+        do R = runs[++k];
+        while (R.cend <= c);
       }
       acc += acc1;
     }

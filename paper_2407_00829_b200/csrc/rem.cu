@@ -65,11 +65,32 @@ __global__ void __launch_bounds__(kRemThreads)
       }
     }
     __syncwarp();
-    for (int r = pk.r0 + lane; r < pk.r1; r += 32) {
-      const int lo = __ldg(P.ptr + r) - pk.e0, hi = __ldg(P.ptr + r + 1) - pk.e0;
+    // lane l sums rows l, l + 32, ...; a row longer than 32 entries is summed
+    // by the whole warp (strided, then a fixed shuffle tree), so a packet's
+    // time does not hang on its longest row
+    for (int r0 = pk.r0; r0 < pk.r1; r0 += 32) {
+      const int r = r0 + lane;
+      int lo = 0, hi = 0;
+      if (r < pk.r1) {
+        lo = __ldg(P.ptr + r) - pk.e0;
+        hi = __ldg(P.ptr + r + 1) - pk.e0;
+      }
+      const bool longr = hi - lo > 32;
       T s = T(0);
-      for (int e = lo; e < hi; ++e) s += prod[e];
-      y[r] = s;
+      if (!longr)
+        for (int e = lo; e < hi; ++e) s += prod[e];
+      unsigned lm = __ballot_sync(kFull, longr);
+      while (lm) {
+        const int q = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const int l2 = __shfl_sync(kFull, lo, q), h2 = __shfl_sync(kFull, hi, q);
+        T t = T(0);
+        for (int e = l2 + lane; e < h2; e += 32) t += prod[e];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
+        if (lane == q) s = t;
+      }
+      if (r < pk.r1) y[r] = s;
     }
   } else {
     // one piece of a long row
