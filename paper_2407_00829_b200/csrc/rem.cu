@@ -37,6 +37,7 @@ template <typename T>
 __global__ void __launch_bounds__(kRemThreads)
     rem_kernel(RemPlan<T> P, const T* __restrict__ x, T* __restrict__ y) {
   __shared__ T prod_s[kWarpsR][kPacketEntries];
+  __shared__ int32_t ptr_s[kWarpsR][kPacketRows + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t wid = (int64_t)blockIdx.x * kWarpsR + warp;
   if (wid >= P.n_packets) return;
@@ -44,7 +45,10 @@ __global__ void __launch_bounds__(kRemThreads)
   if (pk.r1 >= 0) {
     // whole rows [r0, r1): products of their entries, then lane-per-row sums
     T* prod = prod_s[warp];
-    const int n = pk.e1 - pk.e0;
+    int32_t* pt = ptr_s[warp];
+    const int n = pk.e1 - pk.e0, nrow = pk.r1 - pk.r0;
+    // the packet's row pointers, loaded with the first wave of entry loads
+    for (int i = lane; i <= nrow; i += 32) pt[i] = __ldg(P.ptr + pk.r0 + i) - pk.e0;
     for (int w = 0; w < n; w += 32 * kB) {
       int32_t c[kB];
       T v[kB];
@@ -72,8 +76,8 @@ __global__ void __launch_bounds__(kRemThreads)
       const int r = r0 + lane;
       int lo = 0, hi = 0;
       if (r < pk.r1) {
-        lo = __ldg(P.ptr + r) - pk.e0;
-        hi = __ldg(P.ptr + r + 1) - pk.e0;
+        lo = pt[r - pk.r0];
+        hi = pt[r - pk.r0 + 1];
       }
       const bool longr = hi - lo > 32;
       T s = T(0);
