@@ -61,6 +61,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -125,93 +129,104 @@ __device__ __forceinline__ void prefetch_chunk(const unsigned char* stage,
   }
 }
 
+// One bundle of a staged chunk: lane = (item, row r, phase ph of Q) sums
+// columns ph, ph + Q, ... of row r, the phases fold, the row is written (or,
+// for a piece of a split group, summed in `run` / met in global scratch).
 template <typename T>
-__device__ __forceinline__ void compute_chunk(const Plan<T>& P, const unsigned char* stage,
-                                              const T* __restrict__ x, T* __restrict__ y,
-                                              T& run, int lane) {
+__device__ __forceinline__ void process_bundle(const Plan<T>& P, const unsigned char* stage, int b,
+                                               const T* __restrict__ x, T* __restrict__ y,
+                                               T& run, int lane) {
   const ChunkHdr& H = *reinterpret_cast<const ChunkHdr*>(stage);
   const SItem* items = reinterpret_cast<const SItem*>(stage + H.o_item);
   const uint32_t* lmap = reinterpret_cast<const uint32_t*>(stage + H.o_lane);
   const XRun* runs = reinterpret_cast<const XRun*>(stage + H.o_gath);
   const T* val = reinterpret_cast<const T*>(stage + H.o_val);
-  for (int b = 0; b < H.nb; ++b) {
-    const uint32_t m = lmap[b * 32 + lane];
-    const bool valid = (m & kLaneValid) != 0;
-    const int r = (m >> 8) & 31, ph = (m >> 13) & 31, lq = (m >> 18) & 7, Q = 1 << lq;
-    SItem I{};
-    if (valid) I = items[m & 255];
-    const int nr = I.nr;
-    T acc = T(0);
-    if (valid && ph < I.ncol) {
-      // columns ph, ph + Q, ... of row r, run by run (x of column c is
-      // x[off + c] in the run holding c); two accumulators
-      int k = I.xb;
-      XRun R = runs[k];
-      while (R.cend <= ph) R = runs[++k];
-      const T* vp = val + I.v + ph * nr + r;
-      const int step = Q * nr;
-      T acc1 = T(0);
-      int c = ph;
-      for (;;) {
-        const T* xp = x + R.off + c;
-        const int n = (R.cend - c + Q - 1) >> lq;  // this lane's columns in the run
-        int i = 0;
-        for (; i + 3 < n; i += 4) {
-          const T x0 = __ldg(xp), x1 = __ldg(xp + Q), x2 = __ldg(xp + 2 * Q), x3 = __ldg(xp + 3 * Q);
-          acc = fma(vp[0], x0, acc);
-          acc1 = fma(vp[step], x1, acc1);
-          acc = fma(vp[2 * step], x2, acc);
-          acc1 = fma(vp[3 * step], x3, acc1);
-          vp += 4 * step;
-          xp += 4 * Q;
-        }
-        for (; i < n; ++i) {
-          acc = fma(*vp, __ldg(xp), acc);
-          vp += step;
-          xp += Q;
-        }
-        c += n << lq;
-        if (c >= I.ncol) break;
-        do R = runs[++k];
-        while (R.cend <= c);
+  const uint32_t m = lmap[b * 32 + lane];
+  const bool valid = (m & kLaneValid) != 0;
+  const int r = (m >> 8) & 31, ph = (m >> 13) & 31, lq = (m >> 18) & 7, Q = 1 << lq;
+  SItem I{};
+  if (valid) I = items[m & 255];
+  const int nr = I.nr;
+  T acc = T(0);
+  if (valid && ph < I.ncol) {
+    // columns ph, ph + Q, ... of row r, run by run (x of column c is
+    // x[off + c] in the run holding c); two accumulators
+    int k = I.xb;
+    XRun R = runs[k];
+    while (R.cend <= ph) R = runs[++k];
+    const T* vp = val + I.v + ph * nr + r;
+    const int step = Q * nr;
+    T acc1 = T(0);
+    int c = ph;
+    for (;;) {
+      const T* xp = x + R.off + c;
+      const int n = (R.cend - c + Q - 1) >> lq;  // this lane's columns in the run
+      int i = 0;
+      for (; i + 3 < n; i += 4) {
+        const T x0 = __ldg(xp), x1 = __ldg(xp + Q), x2 = __ldg(xp + 2 * Q), x3 = __ldg(xp + 3 * Q);
+        acc = fma(vp[0], x0, acc);
+        acc1 = fma(vp[step], x1, acc1);
+        acc = fma(vp[2 * step], x2, acc);
+        acc1 = fma(vp[3 * step], x3, acc1);
+        vp += 4 * step;
+        xp += 4 * Q;
       }
-      acc += acc1;
-    }
-    // fold the phases: lane ph * nr + r collects ph + 1, ph + 2, ... in order
-    // of a binary tree (fixed by Q and nr: deterministic)
-    const int lqmax = __reduce_max_sync(kFull, (unsigned)(valid ? lq : 0));
-    for (int l = 0; l < lqmax; ++l) {
-      const int d = (1 << l) * nr;
-      const T o = __shfl_sync(kFull, acc, min(lane + d, 31));
-      if (valid && ((ph >> l) & 1) == 0 && ph + (1 << l) < Q) acc += o;
-    }
-    if (valid && ph == 0) {
-      if (!(I.flags & IF_XG)) {
-        run = (I.flags & IF_FIRST) ? acc : run + acc;
-        if (I.flags & IF_LAST) y[I.row0 + r] += run;  // y holds the remainder part
+      for (; i < n; ++i) {
+        acc = fma(*vp, __ldg(xp), acc);
+        vp += step;
+        xp += Q;
       }
+      c += n << lq;
+      if (c >= I.ncol) break;
+      do R = runs[++k];
+      while (R.cend <= c);
     }
-    // a piece of a group shared with another task (alone in its bundle, so
-    // lane 0 holds row 0 of it): meet in global scratch
-    if (__any_sync(kFull, valid && (I.flags & IF_XG))) {
-      const int nr0 = __shfl_sync(kFull, nr, 0), row0 = __shfl_sync(kFull, I.row0, 0);
-      const XgInfo xi = P.xgi[(int64_t)H.i0 + (lmap[b * 32] & 255)];
-      T* sp = P.scratch + xi.slot;
-      if (valid && ph == 0) __stcg(sp + xi.p * 32 + r, acc);
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) last = (atom_add_acq_rel(P.counters + xi.g, 1) + 1 == xi.npieces);
-      last = __shfl_sync(kFull, last, 0);
-      if (last) {
-        if (lane < nr0) {
-          T sum = __ldcg(sp + lane);
-          for (int q = 1; q < xi.npieces; ++q) sum += __ldcg(sp + q * 32 + lane);
-          y[row0 + lane] += sum;
-        }
-        if (lane == 0) P.counters[xi.g] = 0;  // ready for the next launch
-      }
+    acc += acc1;
+  }
+  // fold the phases: lane ph * nr + r collects ph + 1, ph + 2, ... in order
+  // of a binary tree (fixed by Q and nr: deterministic)
+  const int lqmax = __reduce_max_sync(kFull, (unsigned)(valid ? lq : 0));
+  for (int l = 0; l < lqmax; ++l) {
+    const int d = (1 << l) * nr;
+    const T o = __shfl_sync(kFull, acc, min(lane + d, 31));
+    if (valid && ((ph >> l) & 1) == 0 && ph + (1 << l) < Q) acc += o;
+  }
+  if (valid && ph == 0) {
+    if (!(I.flags & IF_XG)) {
+      run = (I.flags & IF_FIRST) ? acc : run + acc;
+      if (I.flags & IF_LAST) y[I.row0 + r] += run;  // y holds the remainder part
     }
   }
+  // a piece of a group shared with another task (alone in its bundle, so
+  // lane 0 holds row 0 of it): meet in global scratch
+  if (__any_sync(kFull, valid && (I.flags & IF_XG))) {
+    const int nr0 = __shfl_sync(kFull, nr, 0), row0 = __shfl_sync(kFull, I.row0, 0);
+    const XgInfo xi = P.xgi[(int64_t)H.i0 + (lmap[b * 32] & 255)];
+    T* sp = P.scratch + xi.slot;
+    if (valid && ph == 0) __stcg(sp + xi.p * 32 + r, acc);
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) last = (atom_add_acq_rel(P.counters + xi.g, 1) + 1 == xi.npieces);
+    last = __shfl_sync(kFull, last, 0);
+    if (last) {
+      if (lane < nr0) {
+        T sum = __ldcg(sp + lane);
+        for (int q = 1; q < xi.npieces; ++q) sum += __ldcg(sp + q * 32 + lane);
+        y[row0 + lane] += sum;
+      }
+      if (lane == 0) P.counters[xi.g] = 0;  // ready for the next launch
+    }
+  }
+
+}
+
+template <typename T>
+__device__ __forceinline__ void compute_chunk(const Plan<T>& P, const unsigned char* stage,
+                                              const T* __restrict__ x, T* __restrict__ y,
+                                              T& run, int lane) {
+  const ChunkHdr& H = *reinterpret_cast<const ChunkHdr*>(stage);
+#pragma unroll 1
+  for (int b = 0; b < H.nb; ++b) process_bundle(P, stage, b, x, y, run, lane);
 }
 
 // ---------------------------------------------------------------- kernel
@@ -275,10 +290,92 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// arch 1: one CTA = kCons consumer warps + a producer warp sharing a ring of
+// stages.  The producer streams the CTA's chunks (one bulk copy each, after
+// the consumers released the stage) and prefetches each landed chunk's x
+// lines into L1; the consumers grab the bundles of the oldest staged chunk
+// with a shared-memory counter and release the stage when it is exhausted.
+constexpr int kCtaThreads = (kCons + 1) * 32;
+
+template <typename T>
+__global__ void __launch_bounds__(kCtaThreads)
+    spmv_cta_kernel(Plan<T> P, const T* __restrict__ x, T* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t kb = P.task[blockIdx.x], ke = P.task[blockIdx.x + 1];
+  const int64_t nk = ke - kb;
+  if (nk <= 0) return;
+  const int NS = P.nstage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);        // [kMaxStages]
+  uint64_t* empty = full + kMaxStages;                        // [kMaxStages]
+  int* next = reinterpret_cast<int*>(empty + kMaxStages);     // [kMaxStages]
+  unsigned char* stages = smem + 256;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(smem_u32(full + s), 1);
+      mbar_init(smem_u32(empty + s), kCons);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kCons) {
+    // ---- producer
+    const uint64_t pol = policy_evict_first();
+    for (int64_t it = 0; it < nk; ++it) {
+      const int s = (int)(it % NS);
+      unsigned char* stage = stages + (size_t)s * P.stage_bytes;
+      ChunkRef ref;
+      if (it >= NS) {
+        mbar_wait(smem_u32(empty + s), (uint32_t)(((it / NS) - 1) & 1));
+        ref = reinterpret_cast<const ChunkHdr*>(stage)->next;  // chunk it, named by chunk it - NS
+      } else {
+        ref = P.cref[kb + it];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        next[s] = 0;
+        issue_chunk(P.stream, ref, stage, smem_u32(full + s), pol);
+      }
+      if (it >= 2 && P.mode != 1) {  // chunk it - 2 has landed: prefetch its x
+        const int sp = (int)((it - 2) % NS);
+        mbar_wait(smem_u32(full + sp), (uint32_t)(((it - 2) / NS) & 1));
+        prefetch_chunk(stages + (size_t)sp * P.stage_bytes, x, lane);
+      }
+    }
+    for (int64_t it = nk - 2 < 0 ? 0 : nk - 2; it < nk && P.mode != 1; ++it) {
+      const int sp = (int)(it % NS);
+      mbar_wait(smem_u32(full + sp), (uint32_t)((it / NS) & 1));
+      prefetch_chunk(stages + (size_t)sp * P.stage_bytes, x, lane);
+    }
+    return;
+  }
+  // ---- consumers
+  T run = T(0);
+  for (int64_t it = 0; it < nk; ++it) {
+    const int s = (int)(it % NS);
+    const unsigned char* stage = stages + (size_t)s * P.stage_bytes;
+    mbar_wait(smem_u32(full + s), (uint32_t)((it / NS) & 1));
+    if (P.mode != 1) {
+      const int nb = reinterpret_cast<const ChunkHdr*>(stage)->nb;
+      for (;;) {
+        int b = 0;
+        if (lane == 0) b = atomicAdd(next + s, 1);
+        b = __shfl_sync(kFull, b, 0);
+        if (b >= nb) break;
+        process_bundle(P, stage, b, x, y, run, lane);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(empty + s));
+  }
+}
+
 }  // namespace
 
 int32_t exec_grid(const sable_handle* h) {
   if (!h || h->n_chunks == 0) return 0;
+  if (h->cfg.arch == 1) return h->cfg.n_tasks;
   return (h->cfg.n_tasks + kWarps - 1) / kWarps;
 }
 
@@ -297,6 +394,20 @@ cudaError_t launch_spmv(const sable_handle* h, const void* x, void* y, cudaStrea
   P.stage_bytes = h->cfg.stage_bytes;
   P.xbuf = h->cfg.xbuf;
   P.mode = h->cfg.mode;
+  if (h->cfg.arch == 1) {
+    const size_t smem = 256 + (size_t)P.nstage * P.stage_bytes;
+    static size_t set_cta[2] = {0, 0};
+    const int tc = sizeof(T) == 8 ? 1 : 0;
+    if (set_cta[tc] < smem) {
+      cudaError_t e = cudaFuncSetAttribute(spmv_cta_kernel<T>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      set_cta[tc] = smem;
+    }
+    spmv_cta_kernel<T><<<(unsigned)exec_grid(h), kCtaThreads, smem, st>>>(
+        P, static_cast<const T*>(x), static_cast<T*>(y));
+    return cudaGetLastError();
+  }
   const size_t smem =
       (size_t)kWarps * warp_smem_bytes(P.nstage, P.stage_bytes, P.xbuf, (int)sizeof(T));
   static size_t set_bytes[2] = {0, 0};

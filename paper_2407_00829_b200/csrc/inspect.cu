@@ -523,6 +523,29 @@ int64_t g_lane_work = 48;  // SABLE_LANE_WORK (plan-time tuning; see item_lq)
 // (tuning and tests).  Invalid overrides -> SABLE_E_INVALID_ARG.
 ExecCfg exec_config(int sv) {
   ExecCfg c;
+  c.arch = (int32_t)env_int("SABLE_ARCH", 1);  // 1 measured faster on C2, C3, C4 (r01)
+  if (c.arch == 1) {
+    // a shared ring per CTA: bigger stages, consumers grab bundles
+    c.stage_bytes = (int32_t)env_int("SABLE_STAGE_BYTES", 12288);
+    c.nstage = (int32_t)env_int("SABLE_NSTAGE", 4);
+    c.item_bytes = (int32_t)env_int("SABLE_ITEM_BYTES", c.stage_bytes - 1024);
+    c.xbuf = 32;
+    const int64_t per_cta = 256 + (int64_t)c.nstage * c.stage_bytes;
+    c.ctas_per_sm = (int32_t)env_int(
+        "SABLE_CTAS_PER_SM", std::max<int64_t>(1, std::min<int64_t>(8, (227 * 1024) / per_cta)));
+    c.mode = (int32_t)env_int("SABLE_EXEC_MODE", 0);
+    c.n_tasks = (int32_t)env_int("SABLE_TASKS", 0);
+    g_lane_work = std::max<int64_t>(1, env_int("SABLE_LANE_WORK", 48));
+    const bool ok = c.stage_bytes % 128 == 0 && c.stage_bytes >= 1024 && c.stage_bytes <= 65536 &&
+                    c.nstage >= 3 && c.nstage <= kMaxStages && c.item_bytes >= 8 * sv &&
+                    c.item_bytes + 512 <= c.stage_bytes && c.ctas_per_sm >= 1 &&
+                    per_cta * c.ctas_per_sm <= 227 * 1024 && c.n_tasks >= 0;
+    if (!ok) {
+      set_error("invalid SABLE_* executor configuration (arch 1 needs nstage >= 3)");
+      throw Fail{SABLE_E_INVALID_ARG};
+    }
+    return c;
+  }
   // defaults: the best of the r01 sweeps on B200 (C2 / C3 / C4)
   c.stage_bytes = (int32_t)env_int("SABLE_STAGE_BYTES", 3072);
   c.nstage = (int32_t)env_int("SABLE_NSTAGE", 2);
@@ -822,7 +845,8 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
   // to the next group boundary when one is near, so only groups larger than a
   // fraction of a task are shared between warps (and combined in scratch)
   const int64_t grid = (int64_t)device_sms() * cfg.ctas_per_sm;
-  const int64_t ntask = cfg.n_tasks > 0 ? cfg.n_tasks : std::max<int64_t>(1, grid * kWarps);
+  const int64_t per_task = cfg.arch == 1 ? 1 : kWarps;  // arch 1: a task per CTA
+  const int64_t ntask = cfg.n_tasks > 0 ? cfg.n_tasks : std::max<int64_t>(1, grid * per_task);
   cfg.n_tasks = (int32_t)ntask;
   std::vector<int64_t> cbytes(nch), cpre(nch + 1, 0);
   for (int64_t k = 0; k < nch; ++k) {
@@ -845,6 +869,9 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
     }
     task[ntask] = (int32_t)nch;
   }
+  if (cfg.arch == 1)  // bundles go to any warp of the CTA: split groups meet in scratch
+    for (auto& it : It)
+      if (it.np > 1) it.flags |= IF_XG;
   for (int64_t t = 1; t < ntask; ++t) {  // groups cut by a task boundary
     const int64_t k = task[t];
     if (k <= 0 || k >= nch) continue;

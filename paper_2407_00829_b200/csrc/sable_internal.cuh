@@ -129,7 +129,10 @@ struct ExecCfg {
   int32_t ctas_per_sm;  // CTAs (kWarps warps each) per SM
   int32_t n_tasks;      // warp tasks = grid * kWarps
   int32_t mode;         // diagnostics: 0 = full; 1 = dense streams only; 2 = remainder only; 3 = dense only
+  int32_t arch;         // 0: a private stage ring per warp; 1: a shared ring per CTA
 };
+
+constexpr int kCons = 8;  // arch 1: consumer warps per CTA (+ one producer warp)
 
 // Shared memory of one warp: mbarriers (256 B) and the stages.
 inline __host__ __device__ uint32_t warp_smem_bytes(int nstage, int stage_bytes, int xbuf, int sv) {

@@ -381,6 +381,10 @@ EXEC_CFGS = {
     "onewarp": dict(SABLE_STAGE_BYTES=2048, SABLE_NSTAGE=4, SABLE_TASKS=1),
     "wide": dict(SABLE_STAGE_BYTES=8192, SABLE_ITEM_BYTES=4096, SABLE_NSTAGE=2, SABLE_XBUF=1024,
                  SABLE_TASKS=3),
+    # the CTA-shared ring (arch 1): default shape, and tiny stages / odd CTA count
+    "cta": dict(SABLE_ARCH=1),
+    "cta_tiny": dict(SABLE_ARCH=1, SABLE_STAGE_BYTES=2048, SABLE_NSTAGE=3, SABLE_ITEM_BYTES=256,
+                     SABLE_TASKS=37),
 }
 
 
@@ -400,7 +404,8 @@ def test_executor_configurations(sable, monkeypatch, cfg):
     for s in cases:
         for split in ("rect", "all_rem"):
             A, _ = check(sable, s, split, exact=s.name in ("rand23", "longrows"))
-            assert A.info["n_tasks"] == EXEC_CFGS[cfg]["SABLE_TASKS"]
+            if "SABLE_TASKS" in EXEC_CFGS[cfg]:
+                assert A.info["n_tasks"] == EXEC_CFGS[cfg]["SABLE_TASKS"]
             A.close()
 
 
