@@ -375,14 +375,16 @@ EXEC_CFGS = {
     # tiny stages and items: every group split into one-column / few-entry
     # pieces, many chunks per warp (the stage ring wraps), and an odd task
     # count that cuts inside groups (pieces meet in global scratch)
-    "tiny": dict(SABLE_STAGE_BYTES=1024, SABLE_ITEM_BYTES=64, SABLE_NSTAGE=2, SABLE_XBUF=64,
+    "tiny": dict(SABLE_ARCH=0, SABLE_STAGE_BYTES=1024, SABLE_ITEM_BYTES=64, SABLE_NSTAGE=2, SABLE_XBUF=64,
                  SABLE_TASKS=997),
     # a single warp walks every chunk (deep ring, running sums)
-    "onewarp": dict(SABLE_STAGE_BYTES=2048, SABLE_NSTAGE=4, SABLE_TASKS=1),
-    "wide": dict(SABLE_STAGE_BYTES=8192, SABLE_ITEM_BYTES=4096, SABLE_NSTAGE=2, SABLE_XBUF=1024,
+    "onewarp": dict(SABLE_ARCH=0, SABLE_STAGE_BYTES=2048, SABLE_NSTAGE=4, SABLE_TASKS=1),
+    "wide": dict(SABLE_ARCH=0, SABLE_STAGE_BYTES=8192, SABLE_ITEM_BYTES=4096, SABLE_NSTAGE=2, SABLE_XBUF=1024,
                  SABLE_TASKS=3),
-    # the CTA-shared ring (arch 1): default shape, and tiny stages / odd CTA count
+    # the CTA-shared ring (arch 1, the default): default shape, one CTA, and
+    # tiny stages / odd CTA count
     "cta": dict(SABLE_ARCH=1),
+    "cta_one": dict(SABLE_ARCH=1, SABLE_TASKS=1),
     "cta_tiny": dict(SABLE_ARCH=1, SABLE_STAGE_BYTES=2048, SABLE_NSTAGE=3, SABLE_ITEM_BYTES=256,
                      SABLE_TASKS=37),
 }
