@@ -96,7 +96,7 @@ def main():
     for lf in sorted(glob.glob(os.path.join(d, "launches_*.csv"))):
         cfg = re.sub(r"^launches_|\.csv$", "", os.path.basename(lf))
         rows = launch_shares(lf)
-        sp = [t for n, t in rows if "spmv_kernel" in n]
+        sp = [t for n, t in rows if "spmv" in n]
         rm = [t for n, t in rows if "rem_kernel" in n]
         lines.append(f"## {cfg}: launch list ({len(rows)} launches)")
         med = lambda v: sorted(v)[len(v) // 2] if v else 0.0  # noqa: E731
