@@ -12,7 +12,9 @@ DESIGN.md "Readings" for the interpretations R1..R18.
 """
 from .oracle import (  # noqa: F401
     OracleError,
+    alg1_cuts,
     build,
+    partition_grid,
     normalize,
     partition,
     rowptr,

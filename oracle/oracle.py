@@ -67,6 +67,8 @@ def _load():
         lib.oracle_spmv_rows.argtypes = [P, P, P, P, C.c_int64, P, P, P]
         lib.oracle_rowptr.restype = None
         lib.oracle_rowptr.argtypes = [C.c_int64, C.c_int64, P, P]
+        lib.oracle_alg1.restype = C.c_int64
+        lib.oracle_alg1.argtypes = [C.c_int64, P, P, C.c_uint32, C.c_uint32, C.c_int32, P]
         _lib = lib
     return _lib
 
@@ -176,3 +178,31 @@ def spmv_rows(rp, J, V, x, rows):
     s = np.empty(len(rows), dtype=np.float64)
     lib.oracle_spmv_rows(_p(rp), _p(J), _p(V), _p(x), len(rows), _p(rows), _p(y), _p(s))
     return y, s
+
+
+def alg1_cuts(n: int, rowptr, J, t_num: int, t_den: int, shifts: bool) -> np.ndarray:
+    """Alg. 1 on a CSR pattern: the grid 0 = g0 < g1 < ...
+    < gk = n (0 followed by the algorithm's cuts), Eq. 1 similarity, or Eq. 2
+    with the +-1 shifts when `shifts`; threshold t_num / t_den, exact."""
+    lib = _load()
+    rp = _c(rowptr, np.int64)
+    J = _c(J, np.int64)
+    cuts = np.zeros(max(n, 1), dtype=np.int32)
+    m = lib.oracle_alg1(n, _p(rp), _p(J), t_num, t_den, 1 if shifts else 0, _p(cuts))
+    return np.concatenate([[0], cuts[:m]]).astype(np.int32)
+
+
+def partition_grid(nrows: int, ncols: int, I, J, t_num: int, t_den: int, shifts: bool):
+    """(rpntr, cpntr) of Alg. 1 for the pattern of COO triples: rows on A,
+    then "the same procedure on the columns" on the pattern of A^T."""
+    I = np.asarray(I, np.int64)
+    J = np.asarray(J, np.int64)
+    o = np.lexsort((J, I))
+    rp = np.zeros(nrows + 1, np.int64)
+    np.cumsum(np.bincount(I, minlength=nrows), out=rp[1:])
+    rows = alg1_cuts(nrows, rp, J[o], t_num, t_den, shifts)
+    o2 = np.lexsort((I, J))
+    cp = np.zeros(ncols + 1, np.int64)
+    np.cumsum(np.bincount(J, minlength=ncols), out=cp[1:])
+    cols = alg1_cuts(ncols, cp, I[o2], t_num, t_den, shifts)
+    return rows, cols

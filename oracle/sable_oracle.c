@@ -380,3 +380,79 @@ void oracle_rowptr(int64_t nrows, int64_t nnz, const int64_t *I, int64_t *rowptr
   for (int64_t k = 0; k < nnz; ++k) rowptr[I[k] + 1]++;
   for (int64_t i = 0; i < nrows; ++i) rowptr[i + 1] += rowptr[i];
 }
+
+/* ---- Alg. 1 "Matrix Partitioning" ---------------------
+ *
+ * PAPER.md:381-416 (Section 5, Algorithm 1), similarity Eq. 1
+ * PAPER.md:358-362 and Eq. 2, over the non-zero PATTERN of
+ * the rows (columns): u.v counts the positions non-zero in both.
+ *
+ *   i <- 0
+ *   while i < n - 1:
+ *     if row i is empty:
+ *       while i < n - 1 and row i+1 is empty: i <- i + 1
+ *       cuts.append(i + 1)
+ *     elif similarity(row i, row i+1) < cut_threshold:
+ *       cuts.append(i + 1)
+ *     i <- i + 1
+ *   cuts.append(n)
+ *
+ * Readings (R17 and R19-R20): Eq. 2's ">>" / "<<"
+ * shift u by one position right / left (column j -> j +- 1, positions
+ * leaving [0, n) dropped) and the similarity takes the maximum of the three
+ * dot products; the threshold is the rational t_num / t_den and the test
+ * "S < t" is evaluated exactly as dot * t_den < t_num * max(nnz u, nnz v);
+ * a cut equal to the previous one (the final append after an empty run that
+ * reaches the last row) is not repeated.  The grid is 0 followed by the cuts.
+ *
+ * The pattern of the "columns" partition is the transpose: call this on the
+ * CSR of A^T.  rowptr/J describe a CSR pattern with columns strictly
+ * increasing per row; cuts receives up to n values; returns their count.
+ */
+static int64_t dot_shift(const int64_t *a, int64_t na, const int64_t *b, int64_t nb,
+                         int64_t shift) {
+  /* #{ j in a : j + shift in b }, both sorted ascending */
+  int64_t i = 0, k = 0, c = 0;
+  while (i < na && k < nb) {
+    const int64_t v = a[i] + shift;
+    if (v < b[k]) ++i;
+    else if (v > b[k]) ++k;
+    else { ++c; ++i; ++k; }
+  }
+  return c;
+}
+
+static int below(const int64_t *rowptr, const int64_t *J, int64_t r, int32_t shifts,
+                 uint32_t t_num, uint32_t t_den) {
+  const int64_t *a = J + rowptr[r], *b = J + rowptr[r + 1];
+  const int64_t na = rowptr[r + 1] - rowptr[r], nb = rowptr[r + 2] - rowptr[r + 1];
+  int64_t dot = dot_shift(a, na, b, nb, 0);
+  if (shifts) {
+    const int64_t dr = dot_shift(a, na, b, nb, 1), dl = dot_shift(a, na, b, nb, -1);
+    if (dr > dot) dot = dr;
+    if (dl > dot) dot = dl;
+  }
+  const int64_t mx = na > nb ? na : nb;
+  return dot * (int64_t)t_den < (int64_t)t_num * mx;
+}
+
+int64_t oracle_alg1(int64_t n, const int64_t *rowptr, const int64_t *J, uint32_t t_num,
+                    uint32_t t_den, int32_t shifts, int32_t *cuts) {
+  int64_t m = 0;
+  int64_t i = 0;
+#define EMPTY(r) (rowptr[(r) + 1] == rowptr[(r)])
+#define APPEND(v) do { if (m == 0 || cuts[m - 1] != (int32_t)(v)) cuts[m++] = (int32_t)(v); } while (0)
+  while (i < n - 1) {
+    if (EMPTY(i)) {
+      while (i < n - 1 && EMPTY(i + 1)) ++i;
+      APPEND(i + 1);
+    } else if (below(rowptr, J, i, shifts, t_num, t_den)) {
+      APPEND(i + 1);
+    }
+    ++i;
+  }
+  APPEND(n);
+#undef EMPTY
+#undef APPEND
+  return m;
+}
