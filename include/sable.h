@@ -235,6 +235,31 @@ sable_status sable_spmv_allgather(sable_handle* h, const void* x_full, void* x_n
 sable_status sable_spmv_iterate(sable_handle* h, void* x_a, void* x_b, int32_t iters,
                                 void* cuda_stream, int32_t* result_in_b);
 
+/* ---- the partitioner ------------------------------
+ * Alg. 1 "Matrix Partitioning" on the device: the row
+ * grid rpntr and column grid cpntr of a CSR matrix, cutting between rows
+ * i and i+1 when S(row i, row i+1) < t, Eq. 1 when
+ * shifts == 0, Eq. 2 (+-1 shifts, reading R17) when
+ * shifts != 0; runs of empty rows extend one block; the
+ * columns are the same procedure on the pattern of A^T.  Readings R19-R21
+ * (DESIGN.md): strictly increasing grids, t = t_num / t_den compared exactly
+ * (dot * t_den < t_num * max(nnz)), no similarity for an empty row i.
+ *   rowptr[nrows+1] (int64, rowptr[0] = 0), colidx[nnz] (int32, strictly
+ *   increasing within a row, < ncols): the pattern; values are not needed.
+ *   mem: where rowptr/colidx live (SABLE_MEM_HOST: copied in; DEVICE: read
+ *   in place, must be device memory of the current device).
+ *   rpntr[nrows+1], cpntr[ncols+1]: HOST buffers (capacity for the finest
+ *   grid) receiving 0 = g0 < ... < gk = n; *nbrows / *nbcols = k.
+ * Synchronises cuda_stream; scratch is stream-ordered and freed on return.
+ * Errors: SABLE_E_INVALID_ARG (NULL, nrows/ncols < 1, t_den == 0, bad mem),
+ * SABLE_E_UNSUPPORTED (sizes >= 2^31), SABLE_E_OOM, SABLE_E_CUDA.  The
+ * pattern is not validated (use sable_vbr_create's validation for that). */
+sable_status sable_partition_grid(int64_t nrows, int64_t ncols, int64_t nnz,
+                                  const int64_t* rowptr, const int32_t* colidx, int32_t mem,
+                                  uint32_t t_num, uint32_t t_den, int32_t shifts,
+                                  void* cuda_stream, int32_t* rpntr, int32_t* nbrows,
+                                  int32_t* cpntr, int32_t* nbcols);
+
 const char* sable_status_string(sable_status s);
 const char* sable_last_error(void); /* thread-local; "" if none */
 int32_t sable_abi_version(void);

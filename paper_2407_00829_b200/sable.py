@@ -33,7 +33,7 @@ EXPORTS = ("sable_vbr_create", "sable_spmv", "sable_spmv_host", "sable_destroy",
            "sable_get_info", "sable_export_partition", "sable_shard_bounds",
            "sable_nccl_unique_id", "sable_comm_init", "sable_spmv_allgather",
            "sable_spmv_iterate", "sable_status_string", "sable_last_error",
-           "sable_abi_version")
+           "sable_abi_version", "sable_partition_grid")
 
 
 class sable_vbr_desc(C.Structure):
@@ -89,6 +89,9 @@ _sig = {
     "sable_comm_init": [_H, _P],
     "sable_spmv_allgather": [_H, _P, _P, _P],
     "sable_spmv_iterate": [_H, _P, _P, C.c_int32, _P, C.POINTER(C.c_int32)],
+    "sable_partition_grid": [C.c_int64, C.c_int64, C.c_int64, _P, _P, C.c_int32, C.c_uint32,
+                             C.c_uint32, C.c_int32, _P, _P, C.POINTER(C.c_int32), _P,
+                             C.POINTER(C.c_int32)],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -177,6 +180,20 @@ def sable_spmv_iterate(h: int, xa_ptr: int, xb_ptr: int, iters: int, stream: int
     _check(_lib.sable_spmv_iterate(_H(h), _P(xa_ptr), _P(xb_ptr), iters, _P(stream), C.byref(r)),
            "sable_spmv_iterate")
     return bool(r.value)
+
+
+def sable_partition_grid(nrows: int, ncols: int, nnz: int, rowptr_ptr: int, colidx_ptr: int,
+                         mem: int, t_num: int, t_den: int, shifts: bool,
+                         stream: int = 0) -> tuple:
+    """Alg. 1 on the device: (rpntr, cpntr) as int32 arrays."""
+    rp = np.zeros(nrows + 1, dtype=np.int32)
+    cp = np.zeros(ncols + 1, dtype=np.int32)
+    nbr, nbc = C.c_int32(0), C.c_int32(0)
+    _check(_lib.sable_partition_grid(nrows, ncols, nnz, _P(rowptr_ptr), _P(colidx_ptr), mem,
+                                     t_num, t_den, 1 if shifts else 0, _P(stream),
+                                     _P(rp.ctypes.data), C.byref(nbr), _P(cp.ctypes.data),
+                                     C.byref(nbc)), "sable_partition_grid")
+    return rp[:nbr.value + 1].copy(), cp[:nbc.value + 1].copy()
 
 
 def sable_status_string(s: int) -> str:
@@ -315,3 +332,24 @@ class VbrMatrix:
             self.close()
         except Exception:
             pass
+
+
+def partition_grid(rowptr, colidx, ncols: int, t_num: int, t_den: int, shifts: bool = True,
+                   stream=None) -> tuple:
+    """Alg. 1 on the GPU for a CSR pattern: rowptr (int64,
+    nrows+1) and colidx (int32), both CUDA tensors or both numpy arrays.
+    Returns (rpntr, cpntr) as int32 numpy arrays (readings R17, R19-R21)."""
+    import torch
+    on_dev = isinstance(rowptr, torch.Tensor) and rowptr.is_cuda
+    if on_dev:
+        rp = rowptr.to(torch.int64).contiguous()
+        ci = colidx.to(torch.int32).contiguous()
+        rp_ptr, ci_ptr, nrows, nnz = rp.data_ptr(), ci.data_ptr(), rp.numel() - 1, ci.numel()
+        mem = SABLE_MEM_DEVICE
+    else:
+        rp = np.ascontiguousarray(rowptr, dtype=np.int64)
+        ci = np.ascontiguousarray(colidx, dtype=np.int32)
+        rp_ptr, ci_ptr, nrows, nnz = rp.ctypes.data, ci.ctypes.data, rp.size - 1, ci.size
+        mem = SABLE_MEM_HOST
+    s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    return sable_partition_grid(nrows, ncols, nnz, rp_ptr, ci_ptr, mem, t_num, t_den, shifts, s)
