@@ -260,6 +260,27 @@ sable_status sable_partition_grid(int64_t nrows, int64_t ncols, int64_t nnz,
                                   void* cuda_stream, int32_t* rpntr, int32_t* nbrows,
                                   int32_t* cpntr, int32_t* nbcols);
 
+/* ---- handle images ---------------------------------
+ * Compile once, run many: the inspected state of a handle
+ * -- executor stream and plan, remainder CSR and packets, panel values, tile
+ * geometry, local cells, scalars incl. the suitability flag of sable_get_info
+ * -- as one byte image ("SABLEVC1": header with an FNV-1a
+ * checksum, then fixed sections 8-byte aligned).  No NCCL state: call
+ * sable_comm_init again on a world > 1 handle.  The image is tied to
+ * SABLE_ABI_VERSION and to the executor configuration it was planned with.
+ *
+ * sable_serialize: buf == NULL (cap ignored) -> *size = image bytes only;
+ * otherwise writes the image to HOST buf (cap >= *size, else
+ * SABLE_E_INVALID_ARG).  Synchronises the handle's device.  Serialising the
+ * same handle twice, or a handle loaded from an image, gives identical bytes.
+ * sable_deserialize: a new handle on the current device from an image of
+ * `size` bytes in host memory (copied; buf may be freed on return).  Errors:
+ * SABLE_E_FORMAT (bad magic, other library version, inconsistent sizes,
+ * checksum mismatch), SABLE_E_OOM, SABLE_E_CUDA. */
+sable_status sable_serialize(const sable_handle* h, void* buf, int64_t cap, int64_t* size);
+sable_status sable_deserialize(const void* buf, int64_t size, void* cuda_stream,
+                               sable_handle** out);
+
 const char* sable_status_string(sable_status s);
 const char* sable_last_error(void); /* thread-local; "" if none */
 int32_t sable_abi_version(void);

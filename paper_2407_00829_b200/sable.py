@@ -33,7 +33,8 @@ EXPORTS = ("sable_vbr_create", "sable_spmv", "sable_spmv_host", "sable_destroy",
            "sable_get_info", "sable_export_partition", "sable_shard_bounds",
            "sable_nccl_unique_id", "sable_comm_init", "sable_spmv_allgather",
            "sable_spmv_iterate", "sable_status_string", "sable_last_error",
-           "sable_abi_version", "sable_partition_grid")
+           "sable_abi_version", "sable_partition_grid", "sable_serialize",
+           "sable_deserialize")
 
 
 class sable_vbr_desc(C.Structure):
@@ -92,6 +93,8 @@ _sig = {
     "sable_partition_grid": [C.c_int64, C.c_int64, C.c_int64, _P, _P, C.c_int32, C.c_uint32,
                              C.c_uint32, C.c_int32, _P, _P, C.POINTER(C.c_int32), _P,
                              C.POINTER(C.c_int32)],
+    "sable_serialize": [_H, _P, C.c_int64, C.POINTER(C.c_int64)],
+    "sable_deserialize": [_P, C.c_int64, _P, C.POINTER(_H)],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -194,6 +197,23 @@ def sable_partition_grid(nrows: int, ncols: int, nnz: int, rowptr_ptr: int, coli
                                      _P(rp.ctypes.data), C.byref(nbr), _P(cp.ctypes.data),
                                      C.byref(nbc)), "sable_partition_grid")
     return rp[:nbr.value + 1].copy(), cp[:nbc.value + 1].copy()
+
+
+def sable_serialize(h: int) -> bytes:
+    """The handle's image (SABLEVC1) as bytes."""
+    n = C.c_int64(0)
+    _check(_lib.sable_serialize(_H(h), None, 0, C.byref(n)), "sable_serialize")
+    buf = (C.c_char * n.value)()
+    _check(_lib.sable_serialize(_H(h), C.cast(buf, _P), n.value, C.byref(n)), "sable_serialize")
+    return bytes(buf)
+
+
+def sable_deserialize(image: bytes, stream: int = 0) -> int:
+    h = _H()
+    buf = C.create_string_buffer(image, len(image))
+    _check(_lib.sable_deserialize(C.cast(buf, _P), len(image), _P(stream), C.byref(h)),
+           "sable_deserialize")
+    return h.value
 
 
 def sable_status_string(s: int) -> str:
@@ -307,6 +327,24 @@ class VbrMatrix:
         s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         in_b = sable_spmv_iterate(self.handle, x_a.data_ptr(), x_b.data_ptr(), iters, s)
         return x_b if in_b else x_a
+
+    # -- images (compile once, run many)
+    def serialize(self) -> bytes:
+        return sable_serialize(self.handle)
+
+    @classmethod
+    def from_image(cls, image: bytes, device=None) -> "VbrMatrix":
+        """A handle loaded from sable_serialize's image, without re-inspection."""
+        import torch
+        self = cls.__new__(cls)
+        self.device = torch.device(device or "cuda")
+        with torch.cuda.device(self.device):
+            self.handle = sable_deserialize(image, torch.cuda.current_stream().cuda_stream)
+        self.info = sable_get_info(self.handle)
+        f64 = self.info["dtype"] == SABLE_F64
+        self.dtype = torch.float64 if f64 else torch.float32
+        self.np_dtype = np.float64 if f64 else np.float32
+        return self
 
     # -- parity export
     def export(self) -> dict:
