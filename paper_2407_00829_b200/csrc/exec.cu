@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads)
 constexpr int kCtaThreads = (kCons + 1) * 32;
 
 template <typename T>
-__global__ void __launch_bounds__(kCtaThreads)
+__global__ void __launch_bounds__(kCtaThreads, cta_regs_occupancy(sizeof(T)))
     spmv_cta_kernel(Plan<T> P, const T* __restrict__ x, T* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -320,14 +320,17 @@ __global__ void __launch_bounds__(kCtaThreads)
   __syncthreads();
 
   if (warp == kCons) {
-    // ---- producer
+    // ---- producer (stage s and ring pass `pass` kept incrementally: no
+    // 64-bit division per chunk)
     const uint64_t pol = policy_evict_first();
-    for (int64_t it = 0; it < nk; ++it) {
-      const int s = (int)(it % NS);
+    const int n = (int)nk;
+    int s = 0, pass = 0;    // chunk it -> stage s, pass = it / NS
+    int sp = 0, passp = 0;  // chunk it - 2 (x prefetch)
+    for (int it = 0; it < n; ++it) {
       unsigned char* stage = stages + (size_t)s * P.stage_bytes;
       ChunkRef ref;
-      if (it >= NS) {
-        mbar_wait(smem_u32(empty + s), (uint32_t)(((it / NS) - 1) & 1));
+      if (pass > 0) {
+        mbar_wait(smem_u32(empty + s), (uint32_t)((pass - 1) & 1));
         ref = reinterpret_cast<const ChunkHdr*>(stage)->next;  // chunk it, named by chunk it - NS
       } else {
         ref = P.cref[kb + it];
@@ -338,24 +341,25 @@ __global__ void __launch_bounds__(kCtaThreads)
         issue_chunk(P.stream, ref, stage, smem_u32(full + s), pol);
       }
       if (it >= 2 && P.mode != 1) {  // chunk it - 2 has landed: prefetch its x
-        const int sp = (int)((it - 2) % NS);
-        mbar_wait(smem_u32(full + sp), (uint32_t)(((it - 2) / NS) & 1));
+        mbar_wait(smem_u32(full + sp), (uint32_t)(passp & 1));
         prefetch_chunk(stages + (size_t)sp * P.stage_bytes, x, lane);
+        if (++sp == NS) { sp = 0; ++passp; }
       }
+      if (++s == NS) { s = 0; ++pass; }
     }
-    for (int64_t it = nk - 2 < 0 ? 0 : nk - 2; it < nk && P.mode != 1; ++it) {
-      const int sp = (int)(it % NS);
-      mbar_wait(smem_u32(full + sp), (uint32_t)((it / NS) & 1));
+    for (int it = n - 2 < 0 ? 0 : n - 2; it < n && P.mode != 1; ++it) {
+      mbar_wait(smem_u32(full + sp), (uint32_t)(passp & 1));
       prefetch_chunk(stages + (size_t)sp * P.stage_bytes, x, lane);
+      if (++sp == NS) { sp = 0; ++passp; }
     }
     return;
   }
   // ---- consumers
   T run = T(0);
-  for (int64_t it = 0; it < nk; ++it) {
-    const int s = (int)(it % NS);
+  int s = 0, pass = 0;
+  for (int it = 0; it < (int)nk; ++it) {
     const unsigned char* stage = stages + (size_t)s * P.stage_bytes;
-    mbar_wait(smem_u32(full + s), (uint32_t)((it / NS) & 1));
+    mbar_wait(smem_u32(full + s), (uint32_t)(pass & 1));
     if (P.mode != 1) {
       const int nb = reinterpret_cast<const ChunkHdr*>(stage)->nb;
       for (;;) {
@@ -368,6 +372,7 @@ __global__ void __launch_bounds__(kCtaThreads)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(empty + s));
+    if (++s == NS) { s = 0; ++pass; }
   }
 }
 
@@ -395,7 +400,7 @@ cudaError_t launch_spmv(const sable_handle* h, const void* x, void* y, cudaStrea
   P.xbuf = h->cfg.xbuf;
   P.mode = h->cfg.mode;
   if (h->cfg.arch == 1) {
-    const size_t smem = 256 + (size_t)P.nstage * P.stage_bytes;
+    const size_t smem = cta_smem_bytes(h->cfg, (int)sizeof(T));
     static size_t set_cta[2] = {0, 0};
     const int tc = sizeof(T) == 8 ? 1 : 0;
     if (set_cta[tc] < smem) {

@@ -530,9 +530,10 @@ ExecCfg exec_config(int sv) {
     c.nstage = (int32_t)env_int("SABLE_NSTAGE", 4);
     c.item_bytes = (int32_t)env_int("SABLE_ITEM_BYTES", c.stage_bytes - 1024);
     c.xbuf = 32;
-    const int64_t per_cta = 256 + (int64_t)c.nstage * c.stage_bytes;
+    const int64_t per_cta = cta_smem_bytes(c, sv);
     c.ctas_per_sm = (int32_t)env_int(
-        "SABLE_CTAS_PER_SM", std::max<int64_t>(1, std::min<int64_t>(8, (227 * 1024) / per_cta)));
+        "SABLE_CTAS_PER_SM",
+        std::max<int64_t>(1, std::min<int64_t>(cta_regs_occupancy(sv), (227 * 1024) / per_cta)));
     c.mode = (int32_t)env_int("SABLE_EXEC_MODE", 0);
     c.n_tasks = (int32_t)env_int("SABLE_TASKS", 0);
     g_lane_work = std::max<int64_t>(1, env_int("SABLE_LANE_WORK", 48));
@@ -545,6 +546,10 @@ ExecCfg exec_config(int sv) {
       throw Fail{SABLE_E_INVALID_ARG};
     }
     return c;
+  }
+  if (c.arch != 0) {
+    set_error("invalid SABLE_ARCH (0 or 1)");
+    throw Fail{SABLE_E_INVALID_ARG};
   }
   // defaults: the best of the r01 sweeps on B200 (C2 / C3 / C4)
   c.stage_bytes = (int32_t)env_int("SABLE_STAGE_BYTES", 3072);

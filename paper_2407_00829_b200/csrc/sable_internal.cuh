@@ -134,6 +134,18 @@ struct ExecCfg {
 
 constexpr int kCons = 8;  // arch 1: consumer warps per CTA (+ one producer warp)
 
+// Resident arch 1 CTAs per SM the registers allow (288 threads: 56 regs
+// for fp32 -> 4, 72 for fp64 -> 3; measured r01: a 4th fp64 CTA that does not
+// fit only adds a tail wave).
+constexpr __host__ __device__ int cta_regs_occupancy(size_t sv) { return sv == 8 ? 3 : 4; }
+
+// Shared memory of one arch 1 CTA: barriers (256 B) and the stages.
+inline __host__ __device__ uint32_t cta_smem_bytes(const ExecCfg& c, int sv) {
+  uint32_t b = 256 + (uint32_t)(c.nstage * c.stage_bytes);
+  (void)sv;
+  return b;
+}
+
 // Shared memory of one warp: mbarriers (256 B) and the stages.
 inline __host__ __device__ uint32_t warp_smem_bytes(int nstage, int stage_bytes, int xbuf, int sv) {
   (void)xbuf;
