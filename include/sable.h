@@ -260,6 +260,22 @@ sable_status sable_partition_grid(int64_t nrows, int64_t ncols, int64_t nnz,
                                   void* cuda_stream, int32_t* rpntr, int32_t* nbrows,
                                   int32_t* cpntr, int32_t* nbcols);
 
+/* ---- multi-vector products ------------------------
+ * Y = A X for k right-hand sides in one pass over the inspected matrix (the
+ * tile stream and the remainder are read once for all k): Y[:, j] = A X[:, j],
+ * y_i = sum_j A_ij x_j per column -- the "user-defined
+ * operation" over the same VBR-C split.
+ *   X: device, row-major ncols x k (the k values of matrix column c at
+ *      X[c*k .. c*k+k)), dtype of the handle; Y: device, row-major
+ *      (row_end - row_begin) x k, fully written; not aliased with X.
+ *   k in {1, 2, 4, 8} (else SABLE_E_UNSUPPORTED).  Asynchronous on
+ *   cuda_stream; the first call allocates k-wide scratch (synchronously).
+ * Each row's sums run in a fixed order (deterministic run to run), within
+ * the SpMV tolerance of the definition, but not bitwise the sable_spmv order.
+ * Needs the default CTA-ring executor plan (SABLE_ARCH=1), else
+ * SABLE_E_UNSUPPORTED. */
+sable_status sable_spmm(sable_handle* h, const void* X, void* Y, int32_t k, void* cuda_stream);
+
 /* ---- handle images ---------------------------------
  * Compile once, run many: the inspected state of a handle
  * -- executor stream and plan, remainder CSR and packets, panel values, tile

@@ -34,7 +34,8 @@ void free_handle(sable_handle* h) {
   void* dev[] = {h->tval,     h->tiles,      h->xt,       h->rem_ptr,
                  h->rem_idx,  h->rem_val,    h->scratch,  h->counters,       h->cell_br,
                  h->cell_bc,  h->cell_cnt,   h->cell_dense, h->tile_canon_off, h->tile_br,
-                 h->br_vbase, h->br_W,       h->xgi,        h->task,       h->cref,       h->stream,     h->x_dev,    h->y_dev};
+                 h->br_vbase, h->br_W,       h->xgi,        h->task,       h->cref,       h->stream,     h->x_dev,    h->y_dev,
+                 h->mm_scratch, h->mm_rscratch};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* rdev[] = {h->rp.packets, h->rp.scratch, h->rp.counters};

@@ -130,6 +130,8 @@ struct ExecCfg {
   int32_t n_tasks;      // warp tasks = grid * kWarps
   int32_t mode;         // diagnostics: 0 = full; 1 = dense streams only; 2 = remainder only; 3 = dense only
   int32_t arch;         // 0: a private stage ring per warp; 1: a shared ring per CTA
+  int32_t rem_grid;     // remainder executor blocks (0: one warp per packet)
+  int32_t pad_;
 };
 
 constexpr int kCons = 8;  // arch 1: consumer warps per CTA (+ one producer warp)
@@ -269,6 +271,10 @@ struct sable_handle {
   // end-to-end staging
   void* x_dev = nullptr;
   void* y_dev = nullptr;
+
+  // multi-vector products (spmm.cu): k-wide scratch, allocated on first use
+  void* mm_scratch = nullptr;
+  void* mm_rscratch = nullptr;
 
   // NCCL
   void* comm = nullptr;

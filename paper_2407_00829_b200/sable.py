@@ -34,7 +34,7 @@ EXPORTS = ("sable_vbr_create", "sable_spmv", "sable_spmv_host", "sable_destroy",
            "sable_nccl_unique_id", "sable_comm_init", "sable_spmv_allgather",
            "sable_spmv_iterate", "sable_status_string", "sable_last_error",
            "sable_abi_version", "sable_partition_grid", "sable_serialize",
-           "sable_deserialize")
+           "sable_deserialize", "sable_spmm")
 
 
 class sable_vbr_desc(C.Structure):
@@ -94,6 +94,7 @@ _sig = {
                              C.c_uint32, C.c_int32, _P, _P, C.POINTER(C.c_int32), _P,
                              C.POINTER(C.c_int32)],
     "sable_serialize": [_H, _P, C.c_int64, C.POINTER(C.c_int64)],
+    "sable_spmm": [_H, _P, _P, C.c_int32, _P],
     "sable_deserialize": [_P, C.c_int64, _P, C.POINTER(_H)],
 }
 for _name, _args in _sig.items():
@@ -199,6 +200,10 @@ def sable_partition_grid(nrows: int, ncols: int, nnz: int, rowptr_ptr: int, coli
     return rp[:nbr.value + 1].copy(), cp[:nbc.value + 1].copy()
 
 
+def sable_spmm(h: int, x_ptr: int, y_ptr: int, k: int, stream: int = 0) -> None:
+    _check(_lib.sable_spmm(_H(h), _P(x_ptr), _P(y_ptr), k, _P(stream)), "sable_spmm")
+
+
 def sable_serialize(h: int) -> bytes:
     """The handle's image (SABLEVC1) as bytes."""
     n = C.c_int64(0)
@@ -212,7 +217,7 @@ def sable_deserialize(image: bytes, stream: int = 0) -> int:
     h = _H()
     buf = C.create_string_buffer(image, len(image))
     _check(_lib.sable_deserialize(C.cast(buf, _P), len(image), _P(stream), C.byref(h)),
-           "sable_deserialize")
+           "sable_deserialize", "sable_spmm")
     return h.value
 
 
@@ -302,6 +307,20 @@ class VbrMatrix:
         s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
         sable_spmv(self.handle, x.data_ptr(), y.data_ptr(), s)
         return y
+
+    def spmm(self, X, Y=None, stream=None):
+        """Y = A X for X of shape (ncols, k), k in {1, 2, 4, 8} (row-major)."""
+        import torch
+        nloc = self.info["row_end"] - self.info["row_begin"]
+        k = X.shape[1]
+        if Y is None:
+            Y = torch.empty((nloc, k), dtype=self.dtype, device=self.device)
+        assert X.dtype == self.dtype and Y.dtype == self.dtype and X.is_cuda and Y.is_cuda
+        assert X.is_contiguous() and Y.is_contiguous() and X.shape[0] == self.info["ncols"]
+        assert Y.shape == (nloc, k)
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        sable_spmm(self.handle, X.data_ptr(), Y.data_ptr(), k, s)
+        return Y
 
     def spmv_host(self, x: np.ndarray, y: np.ndarray | None = None, stream=None) -> np.ndarray:
         import torch
