@@ -69,6 +69,12 @@ __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+__device__ __forceinline__ uint64_t policy_evict_unchanged() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -150,28 +156,17 @@ __device__ __forceinline__ void process_bundle(const Plan<T>& P, const unsigned 
   T acc = T(0);
   if (valid && ph < I.ncol) {
     // columns ph, ph + Q, ... of row r, run by run (x of column c is
-    // x[off + c] in the run holding c); two accumulators
+    // x[off + c] in the run holding c), one accumulator in column order
     int k = I.xb;
     XRun R = runs[k];
     while (R.cend <= ph) R = runs[++k];
     const T* vp = val + I.v + ph * nr + r;
     const int step = Q * nr;
-    T acc1 = T(0);
     int c = ph;
     for (;;) {
       const T* xp = x + R.off + c;
       const int n = (R.cend - c + Q - 1) >> lq;  // this lane's columns in the run
-      int i = 0;
-      for (; i + 3 < n; i += 4) {
-        const T x0 = __ldg(xp), x1 = __ldg(xp + Q), x2 = __ldg(xp + 2 * Q), x3 = __ldg(xp + 3 * Q);
-        acc = fma(vp[0], x0, acc);
-        acc1 = fma(vp[step], x1, acc1);
-        acc = fma(vp[2 * step], x2, acc);
-        acc1 = fma(vp[3 * step], x3, acc1);
-        vp += 4 * step;
-        xp += 4 * Q;
-      }
-      for (; i < n; ++i) {
+      for (int i = 0; i < n; ++i) {
         acc = fma(*vp, __ldg(xp), acc);
         vp += step;
         xp += Q;
@@ -181,7 +176,6 @@ __device__ __forceinline__ void process_bundle(const Plan<T>& P, const unsigned 
       do R = runs[++k];
       while (R.cend <= c);
     }
-    acc += acc1;
   }
   // fold the phases: lane ph * nr + r collects ph + 1, ph + 2, ... in order
   // of a binary tree (fixed by Q and nr: deterministic)
@@ -322,7 +316,7 @@ __global__ void __launch_bounds__(kCtaThreads, cta_regs_occupancy(sizeof(T)))
   if (warp == kCons) {
     // ---- producer (stage s and ring pass `pass` kept incrementally: no
     // 64-bit division per chunk)
-    const uint64_t pol = policy_evict_first();
+    const uint64_t pol = (P.xpf & 2) ? policy_evict_unchanged() : policy_evict_first();
     const int n = (int)nk;
     int s = 0, pass = 0;    // chunk it -> stage s, pass = it / NS
     int sp = 0, passp = 0;  // chunk it - 2 (x prefetch)
@@ -340,14 +334,14 @@ __global__ void __launch_bounds__(kCtaThreads, cta_regs_occupancy(sizeof(T)))
         next[s] = 0;
         issue_chunk(P.stream, ref, stage, smem_u32(full + s), pol);
       }
-      if (it >= 2 && P.mode != 1) {  // chunk it - 2 has landed: prefetch its x
+      if (it >= 2 && P.mode != 1 && (P.xpf & 1)) {  // chunk it - 2 has landed: prefetch its x
         mbar_wait(smem_u32(full + sp), (uint32_t)(passp & 1));
         prefetch_chunk(stages + (size_t)sp * P.stage_bytes, x, lane);
         if (++sp == NS) { sp = 0; ++passp; }
       }
       if (++s == NS) { s = 0; ++pass; }
     }
-    for (int it = n - 2 < 0 ? 0 : n - 2; it < n && P.mode != 1; ++it) {
+    for (int it = n - 2 < 0 ? 0 : n - 2; it < n && P.mode != 1 && (P.xpf & 1); ++it) {
       mbar_wait(smem_u32(full + sp), (uint32_t)(passp & 1));
       prefetch_chunk(stages + (size_t)sp * P.stage_bytes, x, lane);
       if (++sp == NS) { sp = 0; ++passp; }
@@ -399,6 +393,7 @@ cudaError_t launch_spmv(const sable_handle* h, const void* x, void* y, cudaStrea
   P.stage_bytes = h->cfg.stage_bytes;
   P.xbuf = h->cfg.xbuf;
   P.mode = h->cfg.mode;
+  P.xpf = h->cfg.xpf;
   if (h->cfg.arch == 1) {
     const size_t smem = cta_smem_bytes(h->cfg, (int)sizeof(T));
     static size_t set_cta[2] = {0, 0};

@@ -522,7 +522,9 @@ int64_t g_lane_work = 48;  // SABLE_LANE_WORK (plan-time tuning; see item_lq)
 // Executor shape; SABLE_* environment variables override the defaults
 // (tuning and tests).  Invalid overrides -> SABLE_E_INVALID_ARG.
 ExecCfg exec_config(int sv) {
-  ExecCfg c;
+  ExecCfg c{};
+  c.rem_grid = (int32_t)env_int("SABLE_REM_GRID", 0);
+  c.xpf = (int32_t)env_int("SABLE_XPREFETCH", 1);
   c.arch = (int32_t)env_int("SABLE_ARCH", 1);  // 1 measured faster on C2, C3, C4 (r01)
   if (c.arch == 1) {
     // a shared ring per CTA: bigger stages, consumers grab bundles
@@ -1041,19 +1043,28 @@ void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
 template <typename T>
 void plan_remainder(sable_handle* h, const std::vector<int32_t>& H_rp, cudaStream_t st) {
   const int64_t nloc = (int64_t)H_rp.size() - 1;
+  // packet shape (SABLE_REM_ENTRIES / SABLE_REM_ROWS: tuning, <= the shared
+  // buffers of rem_kernel); a row longer than a packet is cut into pieces
+  const int64_t kPE = env_int("SABLE_REM_ENTRIES", kPacketEntries);
+  const int64_t kPR = env_int("SABLE_REM_ROWS", kPacketRows);
+  if (kPE < 32 || kPE > kPacketEntries || kPR < 1 || kPR > kPacketRows) {
+    set_error("invalid SABLE_REM_ENTRIES / SABLE_REM_ROWS");
+    throw Fail{SABLE_E_INVALID_ARG};
+  }
+  const int64_t kPL = std::min<int64_t>(kPieceLen, kPE);
   std::vector<RemPacket> pk;
   int64_t slot = 0, nlong = 0;
   int64_t r = 0;
   while (r < nloc) {
     const int64_t len = (int64_t)H_rp[r + 1] - H_rp[r];
-    if (len > kPieceLen) {
-      const int32_t np = (int32_t)((len + kPieceLen - 1) / kPieceLen);
+    if (len > kPL) {
+      const int32_t np = (int32_t)((len + kPL - 1) / kPL);
       for (int32_t q = 0; q < np; ++q) {
         RemPacket p{};
         p.r0 = (int32_t)r;
         p.r1 = -1 - q;
-        p.e0 = (int32_t)(H_rp[r] + (int64_t)q * kPieceLen);
-        p.e1 = (int32_t)std::min<int64_t>(H_rp[r + 1], (int64_t)p.e0 + kPieceLen);
+        p.e0 = (int32_t)(H_rp[r] + (int64_t)q * kPL);
+        p.e1 = (int32_t)std::min<int64_t>(H_rp[r + 1], (int64_t)p.e0 + kPL);
         p.npieces = np;
         p.slot = (int32_t)slot;
         p.counter = (int32_t)nlong;
@@ -1068,10 +1079,10 @@ void plan_remainder(sable_handle* h, const std::vector<int32_t>& H_rp, cudaStrea
     p.r0 = (int32_t)r;
     p.e0 = H_rp[r];
     int64_t r1 = r;
-    while (r1 < nloc && r1 - r < kPacketRows) {
+    while (r1 < nloc && r1 - r < kPR) {
       const int64_t l1 = (int64_t)H_rp[r1 + 1] - H_rp[r1];
-      if (l1 > kPieceLen) break;
-      if (r1 > r && (int64_t)H_rp[r1 + 1] - H_rp[r] > kPacketEntries) break;
+      if (l1 > kPL) break;
+      if (r1 > r && (int64_t)H_rp[r1 + 1] - H_rp[r] > kPE) break;
       ++r1;
     }
     p.r1 = (int32_t)r1;

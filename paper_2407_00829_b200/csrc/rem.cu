@@ -39,9 +39,10 @@ __global__ void __launch_bounds__(kRemThreads)
   __shared__ T prod_s[kWarpsR][kPacketEntries];
   __shared__ int32_t ptr_s[kWarpsR][kPacketRows + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t wid = (int64_t)blockIdx.x * kWarpsR + warp;
-  if (wid >= P.n_packets) return;
+  for (int64_t wid = (int64_t)blockIdx.x * kWarpsR + warp; wid < P.n_packets;
+       wid += (int64_t)gridDim.x * kWarpsR) {
   const RemPacket pk = P.packets[wid];
+  __syncwarp();  // the previous packet's shared buffers are free
   if (pk.r1 >= 0) {
     // whole rows [r0, r1): products of their entries, then lane-per-row sums
     T* prod = prod_s[warp];
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(kRemThreads)
       P.counters[pk.counter] = 0;  // ready for the next launch
     }
   }
+  }
 }
 
 }  // namespace
@@ -151,7 +153,10 @@ cudaError_t launch_rem(const sable_handle* h, const void* x, void* y, cudaStream
   P.scratch = static_cast<T*>(h->rp.scratch);
   P.counters = h->rp.counters;
   P.n_packets = h->rp.n_packets;
-  const int64_t blocks = (h->rp.n_packets + kWarpsR - 1) / kWarpsR;
+  // one warp per packet, or (SABLE_REM_GRID = blocks > 0) a persistent grid
+  // whose warps stride over the packets
+  int64_t blocks = (h->rp.n_packets + kWarpsR - 1) / kWarpsR;
+  if (h->cfg.rem_grid > 0) blocks = std::min<int64_t>(blocks, h->cfg.rem_grid);
   rem_kernel<T><<<(unsigned)blocks, kRemThreads, 0, st>>>(P, static_cast<const T*>(x),
                                                          static_cast<T*>(y));
   return cudaGetLastError();

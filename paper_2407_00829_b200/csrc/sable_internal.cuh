@@ -131,7 +131,7 @@ struct ExecCfg {
   int32_t mode;         // diagnostics: 0 = full; 1 = dense streams only; 2 = remainder only; 3 = dense only
   int32_t arch;         // 0: a private stage ring per warp; 1: a shared ring per CTA
   int32_t rem_grid;     // remainder executor blocks (0: one warp per packet)
-  int32_t pad_;
+  int32_t xpf;          // arch 1 producer: 1 = prefetch each landed chunk's x lines into L1
 };
 
 constexpr int kCons = 8;  // arch 1: consumer warps per CTA (+ one producer warp)
@@ -166,6 +166,7 @@ struct Plan {
   int32_t* counters;
   int32_t n_tasks;
   int32_t nstage, stage_bytes, xbuf;
+  int32_t xpf;
   int32_t mode;
 };
 
