@@ -25,8 +25,13 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, variant: str = "",
+          extra: tuple = ()) -> str:
+    """Build libsable.so; `variant` + `extra` nvcc flags build an A/B variant
+    libsable_<variant>.so (selected at import with SABLE_LIB=<variant>)."""
     srcs = sources()
+    LIB = os.path.join(PKG, f"libsable_{variant}.so" if variant else "libsable.so")
+    bdir = os.path.join(PKG, "build" + (f"_{variant}" if variant else ""))
     deps = srcs + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "sable.h")]
     if (not force and os.path.exists(LIB)
             and os.path.getmtime(LIB) >= max(os.path.getmtime(p) for p in deps)):
@@ -34,12 +39,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc, lib = _nccl_dirs()
     nvcc = os.environ.get("NVCC", "nvcc")
     objs = []
-    os.makedirs(os.path.join(PKG, "build"), exist_ok=True)
+    os.makedirs(bdir, exist_ok=True)
     for s in srcs:
-        o = os.path.join(PKG, "build", os.path.basename(s) + ".o")
+        o = os.path.join(bdir, os.path.basename(s) + ".o")
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-               "-I", inc, "-c", s, "-o", o]
+               "-I", inc, *extra, "-c", s, "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)
@@ -51,4 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = [a for a in sys.argv[1:] if a not in ("--force", "-v")]
+    # python build.py [--force] [-v] [variant -DFLAG=...]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                variant=args[0] if args else "", extra=tuple(args[1:])))

@@ -36,6 +36,15 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kThreads = kWarps * 32;
 
+// A/B builds: -DSABLE_INNER_UNROLL=N unrolls a lane's column loop N times
+#if defined(SABLE_INNER_UNROLL) && SABLE_INNER_UNROLL > 0
+#define SABLE_STR2(x) #x
+#define SABLE_STR(x) SABLE_STR2(x)
+#define SABLE_INNER_PRAGMA _Pragma(SABLE_STR(unroll SABLE_INNER_UNROLL))
+#else
+#define SABLE_INNER_PRAGMA
+#endif
+
 // ---------------------------------------------------------------- PTX glue
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -166,6 +175,7 @@ __device__ __forceinline__ void process_bundle(const Plan<T>& P, const unsigned 
     for (;;) {
       const T* xp = x + R.off + c;
       const int n = (R.cend - c + Q - 1) >> lq;  // this lane's columns in the run
+      SABLE_INNER_PRAGMA
       for (int i = 0; i < n; ++i) {
         acc = fma(*vp, __ldg(xp), acc);
         vp += step;

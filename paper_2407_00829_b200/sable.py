@@ -14,7 +14,9 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsable.so")
+# SABLE_LIB=<variant> loads an in-tree A/B build libsable_<variant>.so (build.py)
+LIB_PATH = os.path.join(_PKG, f"libsable_{os.environ['SABLE_LIB']}.so" if os.environ.get("SABLE_LIB")
+                        else "libsable.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libsable.so not built at {LIB_PATH}; run __graft_entry__.build()")
