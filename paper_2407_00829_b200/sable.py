@@ -219,7 +219,7 @@ def sable_deserialize(image: bytes, stream: int = 0) -> int:
     h = _H()
     buf = C.create_string_buffer(image, len(image))
     _check(_lib.sable_deserialize(C.cast(buf, _P), len(image), _P(stream), C.byref(h)),
-           "sable_deserialize", "sable_spmm")
+           "sable_deserialize")
     return h.value
 
 
