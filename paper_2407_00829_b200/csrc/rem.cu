@@ -31,7 +31,10 @@ __device__ __forceinline__ int atom_add_acq_rel(int32_t* p, int v) {
 }
 
 constexpr int kWarpsR = kRemThreads / 32;
-constexpr int kB = 8;  // loads per lane in flight
+#ifndef SABLE_REM_KB
+#define SABLE_REM_KB 8
+#endif
+constexpr int kB = SABLE_REM_KB;  // loads per lane in flight (A/B builds: -DSABLE_REM_KB=N)
 
 template <typename T>
 __global__ void __launch_bounds__(kRemThreads)
