@@ -28,7 +28,7 @@ namespace sable {
 
 constexpr int kGroupRows = 32;  // rows per row group (= warp width)
 constexpr int kWarps = 4;       // warps per executor CTA
-constexpr int kMaxStages = 4;   // per-warp stage ring
+constexpr int kMaxStages = 8;   // stage ring depth cap (barrier arrays in the 256-B header)
 
 struct TileDesc {  // export geometry of a dense tile
   int32_t c0;  // first global column of the tile
