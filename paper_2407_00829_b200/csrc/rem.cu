@@ -36,8 +36,12 @@ constexpr int kWarpsR = kRemThreads / 32;
 #endif
 constexpr int kB = SABLE_REM_KB;  // loads per lane in flight (A/B builds: -DSABLE_REM_KB=N)
 
+#ifndef SABLE_REM_MINB
+#define SABLE_REM_MINB 1  // A/B builds: -DSABLE_REM_MINB=N asks for N resident blocks per SM
+#endif
+
 template <typename T>
-__global__ void __launch_bounds__(kRemThreads)
+__global__ void __launch_bounds__(kRemThreads, SABLE_REM_MINB)
     rem_kernel(RemPlan<T> P, const T* __restrict__ x, T* __restrict__ y) {
   __shared__ T prod_s[kWarpsR][kPacketEntries];
   __shared__ int32_t ptr_s[kWarpsR][kPacketRows + 1];
