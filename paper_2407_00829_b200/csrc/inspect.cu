@@ -529,19 +529,22 @@ ExecCfg exec_config(int sv) {
   if (c.arch == 1) {
     // a shared ring per CTA: bigger stages, consumers grab bundles
     c.nstage = (int32_t)env_int("SABLE_NSTAGE", 4);
-    // default stage: the register-limited CTAs per SM share the SM's 228 KB
-    // (1 KB reserved per CTA, 256 B of barriers) -- measured r01: bigger
-    // stages win on C2/C3/C4 (e.g. C4 0.134 -> 0.119 ms for 12 -> 13.9 KB)
-    const int64_t fit = ((228 * 1024) / cta_regs_occupancy(sv) - 1024 - 256) /
+    // default: 3 CTAs per SM (fp32 and fp64) whose stages share the SM's
+    // 228 KB (1 KB reserved per CTA, 256 B of barriers) -- measured r01:
+    // fewer, bigger chunks win (C2 0.054 -> 0.050 ms, C4 0.134 -> 0.113 ms
+    // going from 4 CTAs x 4 x 12 KB to 3 CTAs x 4 x 18.6 KB)
+    const int64_t ctas_dflt = std::min<int64_t>(3, cta_regs_occupancy(sv));
+    const int64_t ctas_env = env_int("SABLE_CTAS_PER_SM", 0);
+    const int64_t fit = ((228 * 1024) / (ctas_env > 0 ? ctas_env : ctas_dflt) - 1024 - 256) /
                         std::max<int64_t>(1, c.nstage);
     c.stage_bytes = (int32_t)env_int("SABLE_STAGE_BYTES",
                                      std::min<int64_t>(65536, fit & ~(int64_t)127));
     c.item_bytes = (int32_t)env_int("SABLE_ITEM_BYTES", c.stage_bytes - 1024);
     c.xbuf = 32;
     const int64_t per_cta = cta_smem_bytes(c, sv);
-    c.ctas_per_sm = (int32_t)env_int(
-        "SABLE_CTAS_PER_SM",
-        std::max<int64_t>(1, std::min<int64_t>(cta_regs_occupancy(sv), (227 * 1024) / per_cta)));
+    c.ctas_per_sm = (int32_t)(ctas_env > 0 ? ctas_env
+                                           : std::max<int64_t>(1, std::min<int64_t>(
+                                                 ctas_dflt, (227 * 1024) / per_cta)));
     c.mode = (int32_t)env_int("SABLE_EXEC_MODE", 0);
     c.n_tasks = (int32_t)env_int("SABLE_TASKS", 0);
     g_lane_work = std::max<int64_t>(1, env_int("SABLE_LANE_WORK", 48));
