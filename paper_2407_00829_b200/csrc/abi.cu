@@ -35,7 +35,8 @@ void free_handle(sable_handle* h) {
                  h->rem_idx,  h->rem_val,    h->scratch,  h->counters,       h->cell_br,
                  h->cell_bc,  h->cell_cnt,   h->cell_dense, h->tile_canon_off, h->tile_br,
                  h->br_vbase, h->br_W,       h->xgi,        h->task,       h->cref,       h->stream,     h->x_dev,    h->y_dev,
-                 h->mm_scratch, h->mm_rscratch};
+                 h->mm_scratch, h->mm_rscratch, h->pv, h->units, h->ubatch, h->xq, h->xside,
+                 h->uxg, h->uscratch, h->ucounters};
   for (void* p : dev)
     if (p) cudaFree(p);
   void* rdev[] = {h->rp.packets, h->rp.scratch, h->rp.counters};

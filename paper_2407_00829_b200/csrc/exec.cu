@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(kCtaThreads, cta_regs_occupancy(sizeof(T)))
 }  // namespace
 
 int32_t exec_grid(const sable_handle* h) {
+  if (h && h->cfg.arch == 2) return (int32_t)((h->n_ubatch + kUnitWarps - 1) / kUnitWarps);
   if (!h || h->n_chunks == 0) return 0;
   if (h->cfg.arch == 1) return h->cfg.n_tasks;
   return (h->cfg.n_tasks + kWarps - 1) / kWarps;
@@ -404,7 +405,7 @@ cudaError_t launch_spmv(const sable_handle* h, const void* x, void* y, cudaStrea
   P.xbuf = h->cfg.xbuf;
   P.mode = h->cfg.mode;
   P.xpf = h->cfg.xpf;
-  if (h->cfg.arch == 1) {
+  if (h->cfg.arch >= 1) {
     const size_t smem = cta_smem_bytes(h->cfg, (int)sizeof(T));
     static size_t set_cta[2] = {0, 0};
     const int tc = sizeof(T) == 8 ? 1 : 0;
@@ -439,7 +440,13 @@ cudaError_t launch_rem(const sable_handle* h, const void* x, void* y, cudaStream
 // y = A x: the remainder executor writes every local row (its remainder
 // sum, or 0), then the dense-tile executor adds the dense part of the rows
 // of block rows with tiles.
+template <typename T>
+cudaError_t launch_units(const sable_handle* h, const void* x, void* y, cudaStream_t st);
+
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st) {
+  if (h->cfg.arch == 2)
+    return h->dtype == SABLE_F64 ? launch_units<double>(h, x, y, st)
+                                 : launch_units<float>(h, x, y, st);
   // diagnostics (SABLE_EXEC_MODE): 2 = remainder executor only, 3 = dense only
   cudaError_t e = cudaSuccess;
   if (h->cfg.mode != 3)

@@ -36,6 +36,12 @@ namespace sable {
 
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st);
 void free_handle(sable_handle* h);
+template <typename T>
+cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vector<int32_t>& H_rpntr,
+                       const std::vector<int32_t>& H_W, const std::vector<int64_t>& br_vbase,
+                       const std::vector<int64_t>& br_wprefix, const std::vector<int64_t>& br_t0,
+                       const std::vector<int32_t>& H_rp, const std::vector<XTile>& H_xt,
+                       cudaStream_t st);
 
 namespace {
 
@@ -525,8 +531,8 @@ ExecCfg exec_config(int sv) {
   ExecCfg c{};
   c.rem_grid = (int32_t)env_int("SABLE_REM_GRID", 0);
   c.xpf = (int32_t)env_int("SABLE_XPREFETCH", 1);
-  c.arch = (int32_t)env_int("SABLE_ARCH", 1);  // 1 measured faster on C2, C3, C4 (r01)
-  if (c.arch == 1) {
+  c.arch = (int32_t)env_int("SABLE_ARCH", 2);  // 2: the unit executor (unit.cu)
+  if (c.arch == 1 || c.arch == 2) {
     // a shared ring per CTA: bigger stages, consumers grab bundles
     c.nstage = (int32_t)env_int("SABLE_NSTAGE", 4);
     // default: 3 CTAs per SM (fp32 and fp64) whose stages share the SM's
@@ -556,10 +562,10 @@ ExecCfg exec_config(int sv) {
       set_error("invalid SABLE_* executor configuration (arch 1 needs nstage >= 3)");
       throw Fail{SABLE_E_INVALID_ARG};
     }
-    return c;
+    return c;  // arch 2 keeps the arch 1 stream for sable_spmm
   }
   if (c.arch != 0) {
-    set_error("invalid SABLE_ARCH (0 or 1)");
+    set_error("invalid SABLE_ARCH (0, 1 or 2)");
     throw Fail{SABLE_E_INVALID_ARG};
   }
   // defaults: the best of the r01 sweeps on B200 (C2 / C3 / C4)
@@ -1516,6 +1522,8 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
   plan_executor<T>(h, cfg, nbl, b0, H_rpntr, H_W, br_vbase, br_wprefix, H_rp, H_xt, st);
   h->cfg = cfg;
   plan_remainder<T>(h, H_rp, st);
+  if (cfg.arch == 2) SB_CU(plan_units<T>(h, nbl, b0, H_rpntr, H_W, br_vbase, br_wprefix, br_t0,
+                                         H_rp, H_xt, st));
 
   // ---- bookkeeping ---------------------------------------------------------------------
   int64_t nnz = 0;

@@ -206,6 +206,63 @@ struct RemHost {
   int64_t n_packets = 0, n_pieces = 0, n_long = 0;
 };
 
+// ---- the unit executor (unit.cu, plan.cu)
+//
+// Dense values of the local block rows as ROW-MAJOR panels `pv`: block row a
+// (h rows, panel width W = the sum of its dense tiles' widths, tiles in bc
+// order) owns rows of Wp = W rounded up to one 16-byte vector (zero padded),
+// row r of the panel at pv[base_a + r * Wp].  A UNIT is one warp's work: a
+// range of <= 32 consecutive rows of one block row with the block row's whole
+// panel (or rows without tiles) and the remainder entries [e0, e1) of those
+// rows.  A unit whose rows are complete writes y once; the pieces of a row
+// range split over several units (rows with very long remainders) meet in
+// scratch, summed in piece order by the last to arrive.
+
+struct Unit {        // 32 B
+  int32_t voff16;    // first value of the unit's first row, in 16-byte vectors
+  int32_t row0;      // first local row
+  int32_t wq;        // dense panel width in 16-byte column vectors (0: no dense part)
+  int32_t xq0;       // the block row's x map: xq[xq0 + q] for column vector q
+  int32_t e0, e1;    // remainder entries of rows [row0, row0 + nr) clamped to [e0, e1)
+  int32_t xg;        // -1: complete rows (write y); else its combine group
+  uint8_t nr;        // rows (1..32)
+  uint8_t llpr;      // log2 of the lanes per row of the dense part (0..5)
+  uint16_t piece;    // piece index inside the combine group
+};
+static_assert(sizeof(Unit) == 32, "Unit is 32 B");
+
+// x map of a panel, one int32 per 16-byte column vector q (panel columns
+// vN .. vN + N - 1, N = 16 / sizeof(T)): c >= 0 -- the vector's columns read
+// x[c], x[c + 1], ... (clamped to ncols - 1: columns past the panel width
+// hold zero values); c < 0 -- the vector straddles a run boundary and its N
+// global columns are xside[~c] (int32 each, N per entry, padded to 16 B).
+
+struct XgU {         // combine group of split units (16 B)
+  int64_t slot;      // scratch base (npieces * 32 partials)
+  int32_t counter;   // arrival counter
+  int32_t npieces;
+};
+
+constexpr int kUnitWarps = 4;        // warps per unit-executor CTA
+constexpr int kRemChunk = 256;       // remainder entries per warp wave (8 per lane)
+
+template <typename T>
+struct UPlan {
+  const Unit* units;
+  const int32_t* batch;   // n_batches + 1 unit boundaries (one batch per warp)
+  const int32_t* xq;      // x maps of the panels
+  const int4* xside;      // columns of straddling vectors
+  const T* pv;
+  const int32_t* rptr;    // local remainder row pointers
+  const int32_t* ridx;
+  const T* rval;
+  const XgU* xg;
+  T* scratch;
+  int32_t* counters;
+  int64_t n_batches;
+  int32_t nm1;            // ncols - 1
+};
+
 // Internal position of element (r, c) of a tile whose first panel column is
 // cs, in a block row of height h, panel width W and panel base vbase.
 __device__ __forceinline__ int64_t panel_pos(int64_t vbase, int64_t W, int64_t h, int64_t cs,
@@ -253,6 +310,22 @@ struct sable_handle {
   void* scratch = nullptr;
   int32_t* counters = nullptr;
   int64_t scratch_elems = 0;
+
+  // unit executor (arch 2)
+  void* pv = nullptr;                // row-major panels
+  int64_t pv_elems = 0;
+  sable::Unit* units = nullptr;
+  int64_t n_units = 0;
+  int32_t* ubatch = nullptr;         // n_ubatch + 1
+  int64_t n_ubatch = 0;
+  int32_t* xq = nullptr;
+  int64_t n_xq = 0;
+  int4* xside = nullptr;
+  int64_t n_xside = 0;
+  sable::XgU* uxg = nullptr;
+  int64_t n_uxg = 0;
+  void* uscratch = nullptr;
+  int32_t* ucounters = nullptr;
 
   // export data (device): local cells and tile geometry
   int32_t* cell_br = nullptr;

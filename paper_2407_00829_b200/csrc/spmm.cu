@@ -355,7 +355,7 @@ extern "C" sable_status sable_spmm(sable_handle* h, const void* X, void* Y, int3
     set_error("sable_spmm: k must be 1, 2, 4 or 8");
     return SABLE_E_UNSUPPORTED;
   }
-  if (h->cfg.arch != 1 && h->n_chunks > 0) {
+  if (h->cfg.arch == 0 && h->n_chunks > 0) {
     set_error("sable_spmm: needs the CTA-ring executor plan (SABLE_ARCH=1, the default)");
     return SABLE_E_UNSUPPORTED;
   }
