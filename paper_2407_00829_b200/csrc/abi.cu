@@ -7,6 +7,9 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -28,6 +31,18 @@ sable_status create_impl(const sable_vbr_desc* d, uint32_t delta, const sable_sh
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st);
 sable_status comm_destroy(sable_handle* h);
 int32_t exec_grid(const sable_handle* h);
+
+cudaError_t set_smem_attr(const void* func, int device, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{func, device}];
+  if (have >= bytes) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
 
 void free_handle(sable_handle* h) {
   if (!h) return;

@@ -531,6 +531,7 @@ ExecCfg exec_config(int sv) {
   ExecCfg c{};
   c.rem_grid = (int32_t)env_int("SABLE_REM_GRID", 0);
   c.xpf = (int32_t)env_int("SABLE_XPREFETCH", 1);
+  c.ustaged = (int32_t)env_int("SABLE_UNIT_STAGED", 0);
   c.arch = (int32_t)env_int("SABLE_ARCH", 2);  // 2: the unit executor (unit.cu)
   if (c.arch == 1 || c.arch == 2) {
     // a shared ring per CTA: bigger stages, consumers grab bundles

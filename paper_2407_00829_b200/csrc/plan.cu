@@ -1,15 +1,20 @@
 // plan.cu -- a5 plan for the unit executor (unit.cu): row-major panels,
-// x runs, units, combine groups and warp batches.
+// x maps, units, combine groups and warp batches.
 //
 // Everything here depends on the local block rows alone -- each block row is
 // planned by itself with fixed budgets -- so a row's units (and with them
 // its summation order) are the same whatever the shard count (north_star
 // s7; reading R12).  Parallelism follows the paper's block-row granularity
 // (PAPER.md:747): a unit never crosses a block row that has dense tiles.
+//
+// Every unit's data (dense rows, x map, remainder row pointers, columns and
+// values, each as its 16-byte-aligned cover) fits one shared-memory stage of
+// the executor (UnitBudget::stage), so the executor can pull a whole unit in
+// with bulk copies while it computes the previous one.
 #include <algorithm>
 #include <climits>
-#include <utility>
 #include <cstdlib>
+#include <utility>
 #include <vector>
 
 #include "sable_internal.cuh"
@@ -41,57 +46,32 @@ int64_t env_i64(const char* name, int64_t dflt) {
   return s && *s ? atoll(s) : dflt;
 }
 
+// Upper bound of the 16-byte-aligned cover of `bytes` bytes.
+constexpr int64_t cover(int64_t bytes) { return bytes > 0 ? bytes + 32 : 0; }
+
 }  // namespace
 
 // Plan budgets (SABLE_U* environment overrides are for tuning runs only).
 struct UnitBudget {
-  int64_t dense_bytes;  // cap on one unit's dense values
-  int64_t piece_ent;    // remainder entries per unit in a split row range
-  int64_t rem_ent;      // remainder entries per remainder-only unit
-  int64_t batch_bytes;  // a warp takes consecutive units up to this many bytes
-  int64_t batch_units;  // ... and at most this many units
-  int64_t unit_cost;    // fixed cost of a unit in lane steps (for the LPR choice)
+  int64_t stage;        // bytes of one unit's data (one executor stage)
+  int64_t rem_rows;     // rows per remainder-only unit (<= 32)
+  int64_t batch_units;  // units per warp batch (the executor's pipeline length)
 };
 
-UnitBudget unit_budget() {
+UnitBudget unit_budget(bool staged) {
   UnitBudget b;
-  b.dense_bytes = env_i64("SABLE_UDENSE", 32768);
-  b.piece_ent = env_i64("SABLE_UPIECE", 2048);
-  b.rem_ent = env_i64("SABLE_UREM", 512);
-  b.batch_bytes = env_i64("SABLE_UBATCH", 16384);
-  b.batch_units = env_i64("SABLE_UBATCH_UNITS", 4);
-  b.unit_cost = env_i64("SABLE_UCOST", 4);
+  b.stage = env_i64("SABLE_USTAGE", staged ? kUnitStage : kUnitBytes);
+  b.rem_rows = std::min<int64_t>(32, std::max<int64_t>(1, env_i64("SABLE_UREM_ROWS", 32)));
+  b.batch_units = std::max<int64_t>(1, env_i64("SABLE_UBATCH_UNITS", 4));
   return b;
 }
 
-// Lanes per row for a panel of Wq column vectors: the smallest power of two
-// covering the panel in one pass, capped at 32 -- every lane then issues all
-// its rows' loads of a pass at once (the executor is latency-bound per unit,
-// so fewer serial passes beat fuller lanes).  SABLE_ULPR_MODE=1 picks the
-// fewest lane steps instead (A/B).
-int choose_llpr(int64_t Wq, int64_t h, const UnitBudget& B) {
-  if (env_i64("SABLE_ULPR_MODE", 0) == 0) {
-    int l = 0;
-    while (l < 5 && (1ll << l) < Wq) ++l;
-    return l;
-  }
-  int best = 5;
-  int64_t best_cost = INT64_MAX;
-  for (int l = 5; l >= 0; --l) {
-    const int64_t L = 1ll << l, sub = 32 / L, K = std::min<int64_t>(L, 8);
-    const int64_t ru = std::min<int64_t>(32, sub * K);
-    const int64_t ng = (h + ru - 1) / ru;
-    int64_t cost = 0;
-    for (int64_t g = 0; g < ng; ++g) {
-      const int64_t nr = h / ng + (g < h % ng ? 1 : 0);
-      cost += ((Wq + L - 1) / L) * ((nr + sub - 1) / sub) + B.unit_cost;
-    }
-    if (cost < best_cost) {
-      best_cost = cost;
-      best = l;
-    }
-  }
-  return best;
+// Lanes per row for a panel of wq column vectors: the smallest power of two
+// covering the panel in one pass, capped at 32.
+int choose_llpr(int64_t wq) {
+  int l = 0;
+  while (l < 5 && (1ll << l) < wq) ++l;
+  return l;
 }
 
 template <typename T>
@@ -100,58 +80,76 @@ cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vect
                        const std::vector<int64_t>& br_wprefix, const std::vector<int64_t>& br_t0,
                        const std::vector<int32_t>& H_rp, const std::vector<XTile>& H_xt,
                        cudaStream_t st) {
-  const int64_t sv = sizeof(T), vec = 16 / sv;
-  const UnitBudget B = unit_budget();
+  const int64_t sv = sizeof(T), vec = 16 / sv, ent = 4 + sv;
+  const UnitBudget B = unit_budget(h->cfg.ustaged != 0);
+  const int64_t S = B.stage;
+  auto rp_bytes = [](int64_t nr) { return cover((nr + 1) * 4); };
+  auto rem_cap = [&](int64_t nr) {  // entries of a remainder-only unit of nr rows
+    return std::max<int64_t>(1, (S - rp_bytes(nr) - 64) / ent);
+  };
+  if (S < 1024 || S % 16 || rem_cap(32) < 32) {
+    set_error("SABLE_USTAGE must be a multiple of 16 and >= 1024");
+    return cudaErrorInvalidValue;
+  }
   std::vector<Unit> U;
-  std::vector<int32_t> xq;       // x map, one entry per column vector
-  std::vector<int32_t> xside;    // 4 columns per straddling column vector
+  std::vector<int32_t> xq;     // x map, one entry per column vector
+  std::vector<int32_t> xside;  // 4 columns per straddling column vector
   std::vector<XgU> xg;
   std::vector<PanelDesc> pd;
   U.reserve(H_rp.size() / 16 + (size_t)nbl + 1);
   int64_t pb = 0, slot = 0;
 
-  // one row range [g0, g1) (local rows) with its dense part, split into
-  // pieces when its remainder is longer than a piece
-  auto emit = [&](int32_t g0, int32_t g1, int32_t wq, int32_t xq0, int64_t voff, int llpr) {
-    const int64_t e0 = H_rp[g0], e1 = H_rp[g1];
-    const int64_t cap = wq > 0 ? B.piece_ent : std::max(B.piece_ent, B.rem_ent);
-    Unit u{};
-    u.row0 = g0;
-    u.nr = (uint8_t)(g1 - g0);
-    u.wq = wq;
-    u.xq0 = xq0;
-    u.voff16 = (int32_t)(voff / vec);
-    u.llpr = (uint8_t)llpr;
-    u.xg = -1;
-    if (e1 - e0 <= cap) {
-      u.e0 = (int32_t)e0;
-      u.e1 = (int32_t)e1;
-      U.push_back(u);
-      return;
+  // A row range's pieces: dense chunks first, then remainder chunks.  One
+  // piece writes y itself; several meet in a combine group (in piece order).
+  std::vector<Unit> pieces;
+  auto flush = [&]() {
+    if (pieces.size() == 1) {
+      pieces[0].xg = -1;
+      U.push_back(pieces[0]);
+    } else if (pieces.size() > 1) {
+      const int32_t g = (int32_t)xg.size();
+      xg.push_back(XgU{slot, g, (int32_t)pieces.size()});
+      slot += (int64_t)pieces.size() * 32;
+      for (size_t p = 0; p < pieces.size(); ++p) {
+        pieces[p].xg = g;
+        pieces[p].piece = (uint16_t)p;
+        U.push_back(pieces[p]);
+      }
     }
-    const int64_t np = (e1 - e0 + cap - 1) / cap;
-    const int32_t g = (int32_t)xg.size();
-    xg.push_back(XgU{slot, g, (int32_t)np});
-    slot += np * 32;
-    for (int64_t p = 0; p < np; ++p) {
-      Unit v = u;
-      v.e0 = (int32_t)(e0 + p * cap);
-      v.e1 = (int32_t)std::min(e1, e0 + (p + 1) * cap);
-      v.xg = g;
-      v.piece = (uint16_t)p;
-      if (p > 0) v.wq = 0;  // the dense part rides on piece 0
-      U.push_back(v);
+    pieces.clear();
+  };
+  // remainder entries [e, e1) of rows [g0, g1) in chunks of `cap`
+  auto rem_pieces = [&](int32_t g0, int32_t g1, int64_t e, int64_t e1, int64_t cap) {
+    for (; e < e1; e += cap) {
+      Unit u{};
+      u.row0 = g0;
+      u.nr = (uint8_t)(g1 - g0);
+      u.e0 = (int32_t)e;
+      u.e1 = (int32_t)std::min(e1, e + cap);
+      pieces.push_back(u);
     }
   };
 
-  // consecutive rows without tiles: groups of <= 32 rows and <= rem_ent
-  // entries; a row longer than that is a group of its own (split in pieces)
+  // consecutive rows without tiles: groups of <= rem_rows rows whose entries
+  // fit a stage; a row longer than that is a group of its own (in pieces)
   auto emit_rem_rows = [&](int32_t r0, int32_t r1) {
     int32_t g0 = r0;
     while (g0 < r1) {
       int32_t g1 = g0 + 1;
-      while (g1 < r1 && g1 - g0 < 32 && (int64_t)H_rp[g1 + 1] - H_rp[g0] <= B.rem_ent) ++g1;
-      emit(g0, g1, 0, 0, 0, 0);
+      while (g1 < r1 && g1 - g0 < B.rem_rows &&
+             (int64_t)H_rp[g1 + 1] - H_rp[g0] <= rem_cap(g1 + 1 - g0))
+        ++g1;
+      const int64_t e0 = H_rp[g0], e1 = H_rp[g1];
+      if (e1 == e0) {
+        Unit u{};
+        u.row0 = g0;
+        u.nr = (uint8_t)(g1 - g0);
+        u.e0 = u.e1 = (int32_t)e0;
+        pieces.push_back(u);
+      } else {
+        rem_pieces(g0, g1, e0, e1, rem_cap(g1 - g0));
+      }
+      flush();
       g0 = g1;
     }
   };
@@ -182,7 +180,7 @@ cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vect
       if (!R.empty() && c0 - tp == R.back().second - R.back().first) continue;
       R.push_back({tp, c0});
     }
-    const int64_t Wq = (W + vec - 1) / vec, Wp = Wq * vec;
+    const int64_t wq = (W + vec - 1) / vec, Wp = wq * vec;
     const int32_t xq0 = (int32_t)xq.size();
     {
       size_t k = 0;
@@ -190,7 +188,7 @@ cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vect
         while (kk + 1 < R.size() && R[kk + 1].first <= f) ++kk;
         return (int32_t)(R[kk].second + (f - R[kk].first));
       };
-      for (int64_t q = 0; q < Wq; ++q) {
+      for (int64_t q = 0; q < wq; ++q) {
         const int64_t f0 = q * vec;
         const int32_t c = col(f0, k);
         const int64_t run_end = k + 1 < R.size() ? R[k + 1].first : W;
@@ -208,43 +206,71 @@ cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vect
       }
     }
     pd.push_back(PanelDesc{br_vbase[la], pb, W, hgt});
-    const int llpr = choose_llpr(Wq, hgt, B);
-    const int64_t L = 1ll << llpr;
-    const int64_t ru = std::min<int64_t>(32, (32 / L) * std::min<int64_t>(L, 8));
-    const int64_t rb = std::max<int64_t>(1, B.dense_bytes / (Wp * sv));
-    const int64_t per = std::min(ru, rb);
-    const int64_t ng = (hgt + per - 1) / per;
-    int64_t g0 = 0;
-    for (int64_t g = 0; g < ng; ++g) {
-      const int64_t nr = hgt / ng + (g < hgt % ng ? 1 : 0);
-      emit(r0 + (int32_t)g0, r0 + (int32_t)(g0 + nr), (int32_t)Wq, xq0, pb + g0 * Wp, llpr);
-      g0 += nr;
+    const int64_t vbase = pb / vec;  // panel base in 16-byte vectors
+    const int64_t row_b = wq * 16;
+    const int64_t xm_b = cover(wq * 4);
+    if (row_b + xm_b + rp_bytes(1) + 64 + ent <= S) {
+      // row groups: as many rows as the lanes' accumulators and a stage hold
+      const int llpr = choose_llpr(wq);
+      const int64_t L = 1ll << llpr;
+      const int64_t ru = std::min<int64_t>(32, (32 / L) * std::min<int64_t>(L, 8));
+      const int64_t rs = std::max<int64_t>(1, (S - xm_b - rp_bytes(32) - 64 - ent) / row_b);
+      const int64_t per = std::min(ru, rs);
+      const int64_t ng = (hgt + per - 1) / per;
+      int64_t g0 = 0;
+      for (int64_t g = 0; g < ng; ++g) {
+        const int64_t nr = hgt / ng + (g < hgt % ng ? 1 : 0);
+        const int32_t a0 = r0 + (int32_t)g0, a1 = a0 + (int32_t)nr;
+        Unit u{};
+        u.row0 = a0;
+        u.nr = (uint8_t)nr;
+        u.wq = (int32_t)wq;
+        u.xq0 = xq0;
+        u.voff16 = (int32_t)(vbase + g0 * wq);
+        u.llpr = (uint8_t)llpr;
+        const int64_t e0 = H_rp[a0], e1 = H_rp[a1];
+        const int64_t room = S - nr * row_b - xm_b - rp_bytes(nr) - 64;
+        const int64_t k0 = std::min<int64_t>(e1 - e0, std::max<int64_t>(0, room / ent));
+        u.e0 = (int32_t)e0;
+        u.e1 = (int32_t)(e0 + k0);
+        pieces.push_back(u);
+        rem_pieces(a0, a1, e0 + k0, e1, rem_cap(nr));
+        flush();
+        g0 += nr;
+      }
+    } else {
+      // a panel wider than a stage: every row in column chunks
+      const int64_t cq = std::max<int64_t>(1, (S - rp_bytes(1) - 64 - 64) / 20);
+      for (int32_t r = 0; r < hgt; ++r) {
+        for (int64_t qa = 0; qa < wq; qa += cq) {
+          const int64_t n = std::min(cq, wq - qa);
+          Unit u{};
+          u.row0 = r0 + r;
+          u.nr = 1;
+          u.wq = (int32_t)n;
+          u.xq0 = xq0 + (int32_t)qa;
+          u.voff16 = (int32_t)(vbase + (int64_t)r * wq + qa);
+          u.llpr = (uint8_t)choose_llpr(n);
+          u.e0 = u.e1 = H_rp[r0 + r];
+          pieces.push_back(u);
+        }
+        rem_pieces(r0 + r, r0 + r + 1, H_rp[r0 + r], H_rp[r0 + r + 1], rem_cap(1));
+        flush();
+      }
     }
     pb += Wp * hgt;
   }
   const int64_t nloc = (int64_t)H_rp.size() - 1;
   if (pend >= 0) emit_rem_rows(pend, (int32_t)nloc);
-  if (pb / vec > INT32_MAX) {
-    set_error("row-major panels exceed 2^31 16-byte vectors");
+  if (pb / vec > INT32_MAX || (int64_t)xq.size() > INT32_MAX || (int64_t)U.size() > INT32_MAX) {
+    set_error("unit plan exceeds 2^31 vectors, x map entries or units");
     return cudaErrorInvalidValue;
   }
 
-  // warp batches: consecutive units up to batch_bytes (at least one unit)
+  // warp batches: runs of consecutive units (a warp pipelines its batch)
   std::vector<int32_t> batch;
-  batch.push_back(0);
-  {
-    int64_t acc = 0, cnt = 0;
-    for (size_t i = 0; i < U.size(); ++i) {
-      const Unit& u = U[i];
-      acc += (int64_t)u.wq * 16 * u.nr + (int64_t)(u.e1 - u.e0) * (sv + 4) + 64;
-      ++cnt;
-      if (acc >= B.batch_bytes || cnt >= B.batch_units || i + 1 == U.size()) {
-        batch.push_back((int32_t)(i + 1));
-        acc = 0;
-        cnt = 0;
-      }
-    }
-  }
+  for (size_t i = 0; i < U.size(); i += (size_t)B.batch_units) batch.push_back((int32_t)i);
+  batch.push_back((int32_t)U.size());
 
   // upload
   cudaError_t e = cudaSuccess;
@@ -254,6 +280,7 @@ cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vect
   h->n_xside = (int64_t)xside.size() / 4;
   h->n_uxg = (int64_t)xg.size();
   h->pv_elems = pb;
+  h->ustage = (int32_t)S;
   auto up = [&](void** dst, const void* src, size_t bytes) {
     if (e) return;
     e = cudaMalloc(dst, bytes ? bytes : 16);

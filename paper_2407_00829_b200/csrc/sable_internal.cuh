@@ -132,6 +132,7 @@ struct ExecCfg {
   int32_t arch;         // 0: a private stage ring per warp; 1: a shared ring per CTA
   int32_t rem_grid;     // remainder executor blocks (0: one warp per packet)
   int32_t xpf;          // arch 1 producer: 1 = prefetch each landed chunk's x lines into L1
+  int32_t ustaged;      // arch 2: 1 = the staged unit executor (bulk copies), 0 = direct loads
 };
 
 constexpr int kCons = 8;  // arch 1: consumer warps per CTA (+ one producer warp)
@@ -244,7 +245,8 @@ struct XgU {         // combine group of split units (16 B)
 };
 
 constexpr int kUnitWarps = 4;        // warps per unit-executor CTA
-constexpr int kRemChunk = 256;       // remainder entries per warp wave (8 per lane)
+constexpr int kUnitStage = 4096;     // bytes of one stage of the staged executor
+constexpr int kUnitBytes = 32768;    // default cap on one unit's data (direct executor)
 
 template <typename T>
 struct UPlan {
@@ -261,6 +263,8 @@ struct UPlan {
   int32_t* counters;
   int64_t n_batches;
   int32_t nm1;            // ncols - 1
+  int32_t pf;             // 1: bulk L2 prefetch of the next unit's data
+  uint32_t stage;         // bytes of one stage (a unit's data)
 };
 
 // Internal position of element (r, c) of a tile whose first panel column is
@@ -271,6 +275,10 @@ __device__ __forceinline__ int64_t panel_pos(int64_t vbase, int64_t W, int64_t h
   const int64_t nr = (h - g * kGroupRows) < kGroupRows ? (h - g * kGroupRows) : kGroupRows;
   return vbase + g * kGroupRows * W + (cs + c) * nr + (r - g * kGroupRows);
 }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+// for at least `bytes` (thread-safe).
+cudaError_t set_smem_attr(const void* func, int device, size_t bytes);
 
 // Thread-local error text for sable_last_error().
 void set_error(const std::string& msg);
@@ -326,6 +334,7 @@ struct sable_handle {
   int64_t n_uxg = 0;
   void* uscratch = nullptr;
   int32_t* ucounters = nullptr;
+  int32_t ustage = 0;                // bytes of a unit's stage (plan.cu)
 
   // export data (device): local cells and tile geometry
   int32_t* cell_br = nullptr;
