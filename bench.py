@@ -245,8 +245,12 @@ def run_sable(args):
     torch.cuda.synchronize()
     e2e_ms = statistics.mean(a.elapsed_time(b) for a, b in e2e_ev)
 
-    # our kernels per step: the remainder executor and the dense-tile executor
-    launches_per_step = int(info["rem_packets"] > 0) + int(info["n_items"] > 0)
+    # our kernels per step: one unit-executor launch (arch 2), or the legacy
+    # remainder + dense-tile executors
+    if info["arch"] == 2:
+        launches_per_step = int(info["n_unit_batches"] > 0)
+    else:
+        launches_per_step = int(info["rem_packets"] > 0) + int(info["n_items"] > 0)
     red = torch.tensor([ms, k_ms, e2e_ms, info["bytes_alg"]], dtype=torch.float64, device=dev)
     if world > 1:
         mx = red.clone()
@@ -282,11 +286,11 @@ def run_sable(args):
                 "grid": [len(s.rpntr) - 1, len(s.cpntr) - 1],
                 "n_cells": info["n_cells"], "n_dense_tiles": info["n_dense"],
                 "tile_elems": info["tile_elems"], "rem_nnz": info["rem_nnz"],
-                "work_items": info["n_items"], "n_tasks": info["n_tasks"],
-                "n_chunks": info["n_chunks"], "n_bundles": info["n_bundles"],
-                "bundle_lane_fill": round(info["n_bundle_lanes"] / max(1, 32 * info["n_bundles"]), 3),
-                "stream_bytes": info["stream_bytes"], "rem_packets": info["rem_packets"],
-                "exec_grid": info["exec_grid"], "item_bytes": info["item_bytes"],
+                "executor": ("unit (arch 2, staged)" if info["unit_staged"] else "unit (arch 2)")
+                if info["arch"] == 2 else f"legacy stream (arch {info['arch']})",
+                "n_units": info["n_units"], "warps": info["n_unit_batches"],
+                "n_combine": info["n_combine"], "panel_elems": info["panel_elems"],
+                "xmap_entries": info["xmap_entries"], "exec_grid": info["exec_grid"],
                 "l2": ("flushed between timed steps (512 MiB write, then read)" if flush_l2 else
                        "not flushed: working set > L2 (iterated SpMV, cache behaviour is real)"),
                 "parallelism": f"row-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
@@ -296,7 +300,8 @@ def run_sable(args):
                 "bound": "hbm", "achieved": round(ach, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic_for(args.config),
                 "peak_kind": peak_kind,
-                "kernel": "one SpMV = sable::rem_kernel + sable::spmv_kernel (back to back)",
+                "kernel": ("one SpMV = one sable::unit_kernel launch" if info["arch"] == 2 else
+                           "one SpMV = sable::rem_kernel + sable::spmv_cta_kernel"),
                 "kernel_ms": round(k_ms, 6),
                 "bytes_alg_per_launch": bytes_alg_local_max,
             },
@@ -309,7 +314,7 @@ def run_sable(args):
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(s, budget_s=args.cpu_budget)
+            line["cpu_baseline"] = cpu_baseline(s)
         print(json.dumps(line), flush=True)
     A.close()
     if world > 1:
@@ -318,66 +323,104 @@ def run_sable(args):
 
 # --------------------------------------------------------------- oracle timing
 
+def host_info():
+    """nproc and the CPU model of this host."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
 def oracle_sample(s, max_nnz: int):
     """The first rows of the matrix holding at most max_nnz non-zeros."""
     rp = s.rowptr()
     r = int(np.searchsorted(rp, max_nnz, side="right") - 1)
     r = max(1, min(r, s.nrows))
     k = int(rp[r])
-    return r, k
+    return r, k, rp[: r + 1]
 
 
-def cpu_baseline(s, budget_s: float = 10.0, max_nnz: int = 12_000_000):
-    """The oracle's fp64 SpMV (oracle_spmv, single-threaded plain C) on a
-    bounded sample of the same matrix, timed on this host."""
+def time_oracle(rp, J, V, x, r, nthreads, reps=5, budget_s=20.0):
+    """Median ms of `reps` oracle SpMVs (after one warm-up), fewer if the
+    budget runs out."""
     import oracle
-    r, k = oracle_sample(s, max_nnz)
-    I, J = s.I[:k], s.J[:k]
-    V = s.V[:k].astype(np.float64)
-    x = s.x.astype(np.float64)
-    oracle.spmv(r, I, J, V, x)  # warm-up
-    reps, t0 = 0, time.perf_counter()
-    while True:
-        oracle.spmv(r, I, J, V, x)
-        reps += 1
-        dt = time.perf_counter() - t0
-        if dt > budget_s or reps >= 50:
+    oracle.spmv_csr_mt(rp, J, V, x, r, nthreads)  # warm-up
+    ts = []
+    t_all = time.perf_counter()
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.spmv_csr_mt(rp, J, V, x, r, nthreads)
+        ts.append((time.perf_counter() - t0) * 1e3)
+        if time.perf_counter() - t_all > budget_s:
             break
-    per = dt / reps
-    return {"value": round(2.0 * k / per / 1e9, 4), "unit": "GFLOP/s", "cores": 1,
-            "kind": "oracle",
-            "sample": f"oracle_spmv (fp64, 1 thread) over rows [0,{r}) = {k} of {s.nnz} nnz, "
-                      f"{reps} reps, {per * 1e3:.1f} ms/rep"}
+    return statistics.median(ts), len(ts)
+
+
+def cpu_baseline(s, max_nnz: int = 64_000_000, partition: bool = True):
+    """The oracle's fp64 SpMV (plain C, oracle/sable_oracle.c) on this host:
+    median of 5 after a warm-up, single-threaded and row-parallel on all
+    cores (OpenMP; bitwise the same y), on the first rows of the matrix
+    holding <= max_nnz non-zeros (all of C1..C4); plus the oracle's
+    partition time next to the GPU inspector's."""
+    import oracle
+    nproc, model = host_info()
+    r, k, rp = oracle_sample(s, max_nnz)
+    J = np.ascontiguousarray(s.J[:k], dtype=np.int64)
+    V = np.ascontiguousarray(s.V[:k], dtype=np.float64)
+    x = s.x.astype(np.float64)
+    ms1, n1 = time_oracle(rp, J, V, x, r, 1)
+    msn, nn = time_oracle(rp, J, V, x, r, nproc)
+    out = {"value": round(2.0 * k / (msn * 1e-3) / 1e9, 4), "unit": "GFLOP/s", "cores": nproc,
+           "kind": "oracle",
+           "sample": f"oracle_spmv_csr_mt (fp64) over rows [0,{r}) = {k} of {s.nnz} nnz; "
+                     f"median of {nn} after 1 warm-up, {nproc} OpenMP threads: {msn:.2f} ms",
+           "single_thread": {"value": round(2.0 * k / (ms1 * 1e-3) / 1e9, 4), "unit": "GFLOP/s",
+                             "ms": round(ms1, 3), "reps": n1},
+           "all_cores_ms": round(msn, 3), "nproc": nproc, "cpu_model": model}
+    if partition:
+        t0 = time.perf_counter()
+        oracle.partition(s.nrows, s.ncols, s.I, s.J, s.V.astype(np.float64), s.rpntr, s.cpntr,
+                         s.delta)
+        out["oracle_partition_ms"] = round((time.perf_counter() - t0) * 1e3, 1)
+    return out
 
 
 def run_reference(args):
-    """--impl reference: the oracle as it stands, on the host cores."""
+    """--impl reference: the oracle as it stands, on all host cores (OpenMP,
+    row-parallel; the reference arm of this tier is the oracle)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
     s, _, _ = make_input(args.config)
-    r, k = oracle_sample(s, 8_000_000)
-    I, J = s.I[:k], s.J[:k]
-    V = s.V[:k].astype(np.float64)
+    nproc, model = host_info()
+    r, k, rp = oracle_sample(s, 64_000_000)
+    J = np.ascontiguousarray(s.J[:k], dtype=np.int64)
+    V = np.ascontiguousarray(s.V[:k], dtype=np.float64)
     x = s.x.astype(np.float64)
     for _ in range(args.warmup):
-        oracle.spmv(r, I, J, V, x)
+        oracle.spmv_csr_mt(rp, J, V, x, r, nproc)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.spmv(r, I, J, V, x)
+        oracle.spmv_csr_mt(rp, J, V, x, r, nproc)
     ms = (time.perf_counter() - t0) * 1e3 / args.steps
     v = 2.0 * k / (ms * 1e-3) / 1e9
-    sample = f"oracle_spmv (fp64, 1 thread) over rows [0,{r}) = {k} of {s.nnz} nnz per step"
+    sample = (f"oracle_spmv_csr_mt (fp64, {nproc} OpenMP threads) over rows [0,{r}) = {k} of "
+              f"{s.nnz} nnz per step")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GFLOP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "config": {"workload": f"{args.config} -- {WORKLOADS[args.config]}",
                                                          "n": s.nrows, "nnz": s.nnz},
-        "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": 1, "kind": "oracle",
-                         "sample": sample},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": nproc, "kind": "oracle",
+                         "sample": sample, "cpu_model": model},
         "e2e": {"value": round(v, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -388,9 +431,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="sable", choices=["sable", "reference"])
-    ap.add_argument("--cpu-budget", type=float, default=5.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

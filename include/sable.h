@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SABLE_ABI_VERSION 1
+#define SABLE_ABI_VERSION 2
 
 typedef struct sable_handle sable_handle;
 
@@ -142,6 +142,14 @@ typedef struct {
   int64_t n_bundles;          /* dense executor lane maps (bundles)           */
   int64_t stream_bytes;       /* bytes of the dense executor stream           */
   int64_t n_bundle_lanes;     /* lanes with work summed over the bundles      */
+  /* the unit executor (SABLE_ARCH=2, the default) */
+  int32_t arch;               /* executor of sable_spmv: 2 = units, 1/0 = legacy stream */
+  int32_t unit_staged;        /* 1: units pulled through shared-memory stages  */
+  int64_t n_units;            /* warp work units (<= 32 rows of one block row) */
+  int64_t n_unit_batches;     /* warps of one sable_spmv launch                */
+  int64_t n_combine;          /* row ranges split over several units          */
+  int64_t panel_elems;        /* row-major panel elements (16-byte padded rows) */
+  int64_t xmap_entries;       /* x map entries (one per 16-byte column vector) */
 } sable_info;
 
 /* Caller-allocated HOST buffers for sable_export_partition, sized from

@@ -18,6 +18,7 @@ from .oracle import (  # noqa: F401
     normalize,
     partition,
     rowptr,
+    spmv_csr_mt,
     spmv,
     spmv_rows,
 )

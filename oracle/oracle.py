@@ -28,7 +28,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle shared library in-tree (gcc, fp64, no contraction)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-std=c11", "-Wall",
-                               "-shared", "-fPIC", "-o", _LIB, _SRC, "-lm"])
+                               "-fopenmp", "-shared", "-fPIC", "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
 
@@ -65,6 +65,8 @@ def _load():
         lib.oracle_spmv.argtypes = [C.c_int64, C.c_int64, P, P, P, P, P, P]
         lib.oracle_spmv_rows.restype = None
         lib.oracle_spmv_rows.argtypes = [P, P, P, P, C.c_int64, P, P, P]
+        lib.oracle_spmv_csr_mt.restype = None
+        lib.oracle_spmv_csr_mt.argtypes = [P, P, P, P, C.c_int64, C.c_int32, P, P]
         lib.oracle_rowptr.restype = None
         lib.oracle_rowptr.argtypes = [C.c_int64, C.c_int64, P, P]
         lib.oracle_alg1.restype = C.c_int64
@@ -177,6 +179,19 @@ def spmv_rows(rp, J, V, x, rows):
     y = np.empty(len(rows), dtype=np.float64)
     s = np.empty(len(rows), dtype=np.float64)
     lib.oracle_spmv_rows(_p(rp), _p(J), _p(V), _p(x), len(rows), _p(rows), _p(y), _p(s))
+    return y, s
+
+
+def spmv_csr_mt(rp, J, V, x, nrows: int, nthreads: int):
+    """y, s for rows [0, nrows) on `nthreads` OpenMP threads (timing only)."""
+    lib = _load()
+    rp = _c(rp, np.int64)
+    J = _c(J, np.int64)
+    V = _c(V, np.float64)
+    x = _c(x, np.float64)
+    y = np.empty(nrows, dtype=np.float64)
+    s = np.empty(nrows, dtype=np.float64)
+    lib.oracle_spmv_csr_mt(_p(rp), _p(J), _p(V), _p(x), nrows, nthreads, _p(y), _p(s))
     return y, s
 
 

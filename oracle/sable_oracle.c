@@ -374,6 +374,25 @@ void oracle_spmv_rows(const int64_t *rowptr, const int64_t *J, const double *V,
   }
 }
 
+/* The same definition for rows [0, nrows) split across `nthreads` OpenMP
+ * threads (row-parallel; every row keeps its own order, so y and s are
+ * bitwise those of oracle_spmv_rows).  Used only to time the oracle on all
+ * host cores (bench.py's cpu_baseline). */
+void oracle_spmv_csr_mt(const int64_t *rowptr, const int64_t *J, const double *V,
+                        const double *x, int64_t nrows, int32_t nthreads, double *y,
+                        double *s) {
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+  for (int64_t i = 0; i < nrows; ++i) {
+    double acc = 0.0, sc = 0.0;
+    for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+      acc += V[k] * x[J[k]];
+      sc += fabs(V[k]) * fabs(x[J[k]]);
+    }
+    y[i] = acc;
+    s[i] = sc;
+  }
+}
+
 /* COO row pointer of the normalised triples (a counting pass). */
 void oracle_rowptr(int64_t nrows, int64_t nnz, const int64_t *I, int64_t *rowptr) {
   for (int64_t i = 0; i <= nrows; ++i) rowptr[i] = 0;

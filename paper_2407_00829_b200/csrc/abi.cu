@@ -260,6 +260,13 @@ sable_status sable_get_info(const sable_handle* h, sable_info* info) {
   info->n_bundles = h->n_bundles;
   info->stream_bytes = h->stream_bytes;
   info->n_bundle_lanes = h->n_bundle_lanes;
+  info->arch = h->cfg.arch;
+  info->unit_staged = h->cfg.ustaged;
+  info->n_units = h->n_units;
+  info->n_unit_batches = h->n_ubatch;
+  info->n_combine = h->n_uxg;
+  info->panel_elems = h->pv_elems;
+  info->xmap_entries = h->n_xq;
   return SABLE_OK;
 }
 

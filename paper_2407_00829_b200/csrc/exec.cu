@@ -415,7 +415,7 @@ cudaError_t launch_spmv(const sable_handle* h, const void* x, void* y, cudaStrea
       if (e != cudaSuccess) return e;
       set_cta[tc] = smem;
     }
-    spmv_cta_kernel<T><<<(unsigned)exec_grid(h), kCtaThreads, smem, st>>>(
+    spmv_cta_kernel<T><<<(unsigned)h->cfg.n_tasks, kCtaThreads, smem, st>>>(
         P, static_cast<const T*>(x), static_cast<T*>(y));
     return cudaGetLastError();
   }

@@ -244,7 +244,10 @@ struct XgU {         // combine group of split units (16 B)
   int32_t npieces;
 };
 
-constexpr int kUnitWarps = 4;        // warps per unit-executor CTA
+#ifndef SABLE_UNIT_WARPS
+#define SABLE_UNIT_WARPS 1  // A/B builds: warps per unit-executor CTA (1: measured r02)
+#endif
+constexpr int kUnitWarps = SABLE_UNIT_WARPS;
 constexpr int kUnitStage = 4096;     // bytes of one stage of the staged executor
 constexpr int kUnitBytes = 32768;    // default cap on one unit's data (direct executor)
 

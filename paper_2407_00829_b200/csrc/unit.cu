@@ -44,9 +44,10 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kUnitThreads = kUnitWarps * 32;
-#ifndef SABLE_UNIT_MINB
-#define SABLE_UNIT_MINB 6  // A/B builds: resident CTAs per SM asked of ptxas
+#ifndef SABLE_UNIT_MINW
+#define SABLE_UNIT_MINW 32  // A/B builds: resident warps per SM asked of ptxas (64 regs)
 #endif
+constexpr int kUnitMinBlocks = SABLE_UNIT_MINW / kUnitWarps;
 
 template <typename T>
 struct Vec;
@@ -296,7 +297,7 @@ __device__ __forceinline__ T rem_rows(const UPlan<T>& P, const Unit& U, const T*
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kUnitThreads, SABLE_UNIT_MINB)
+__global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
     unit_kernel(const __grid_constant__ UPlan<T> P, const T* __restrict__ x, T* __restrict__ y) {
   __shared__ __align__(16) T buf_s[kUnitWarps][kRemWave];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -569,7 +570,7 @@ __host__ __device__ constexpr uint32_t staged_warp_bytes(uint32_t stage) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kUnitThreads, SABLE_UNIT_MINB)
+__global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
     unit_staged_kernel(const __grid_constant__ UPlan<T> P, const T* __restrict__ x,
                        T* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char smem[];

@@ -68,7 +68,10 @@ class sable_info(C.Structure):
                 ("n_tasks", C.c_int64), ("exec_grid", C.c_int32), ("item_bytes", C.c_int32),
                 ("rem_packets", C.c_int64), ("rem_long_pieces", C.c_int64),
                 ("n_chunks", C.c_int64), ("n_bundles", C.c_int64), ("stream_bytes", C.c_int64),
-                ("n_bundle_lanes", C.c_int64)]
+                ("n_bundle_lanes", C.c_int64),
+                ("arch", C.c_int32), ("unit_staged", C.c_int32), ("n_units", C.c_int64),
+                ("n_unit_batches", C.c_int64), ("n_combine", C.c_int64),
+                ("panel_elems", C.c_int64), ("xmap_entries", C.c_int64)]
 
 
 class sable_partition_host(C.Structure):

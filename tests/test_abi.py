@@ -46,7 +46,7 @@ def test_library_is_sm100a(sable):
 
 
 def test_status_strings_and_version(sable):
-    assert sable.sable_abi_version() == 1
+    assert sable.sable_abi_version() == 2
     assert sable.sable_status_string(0) == "SABLE_OK"
     assert sable.sable_status_string(sable.SABLE_E_DUPLICATE) == "SABLE_E_DUPLICATE"
 
