@@ -245,12 +245,8 @@ def run_sable(args):
     torch.cuda.synchronize()
     e2e_ms = statistics.mean(a.elapsed_time(b) for a, b in e2e_ev)
 
-    # our kernels per step: one unit-executor launch (arch 2), or the legacy
-    # remainder + dense-tile executors
-    if info["arch"] == 2:
-        launches_per_step = int(info["n_unit_batches"] > 0)
-    else:
-        launches_per_step = int(info["rem_packets"] > 0) + int(info["n_items"] > 0)
+    # our kernels per step: one unit-executor launch (sable::unit_kernel)
+    launches_per_step = int(info["n_unit_batches"] > 0)
     red = torch.tensor([ms, k_ms, e2e_ms, info["bytes_alg"]], dtype=torch.float64, device=dev)
     if world > 1:
         mx = red.clone()
@@ -286,8 +282,7 @@ def run_sable(args):
                 "grid": [len(s.rpntr) - 1, len(s.cpntr) - 1],
                 "n_cells": info["n_cells"], "n_dense_tiles": info["n_dense"],
                 "tile_elems": info["tile_elems"], "rem_nnz": info["rem_nnz"],
-                "executor": ("unit (arch 2, staged)" if info["unit_staged"] else "unit (arch 2)")
-                if info["arch"] == 2 else f"legacy stream (arch {info['arch']})",
+                "executor": "unit executor (one launch per SpMV)",
                 "n_units": info["n_units"], "warps": info["n_unit_batches"],
                 "n_combine": info["n_combine"], "panel_elems": info["panel_elems"],
                 "xmap_entries": info["xmap_entries"], "exec_grid": info["exec_grid"],
@@ -300,8 +295,7 @@ def run_sable(args):
                 "bound": "hbm", "achieved": round(ach, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic_for(args.config),
                 "peak_kind": peak_kind,
-                "kernel": ("one SpMV = one sable::unit_kernel launch" if info["arch"] == 2 else
-                           "one SpMV = sable::rem_kernel + sable::spmv_cta_kernel"),
+                "kernel": "one SpMV = one sable::unit_kernel launch",
                 "kernel_ms": round(k_ms, 6),
                 "bytes_alg_per_launch": bytes_alg_local_max,
             },

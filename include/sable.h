@@ -127,29 +127,19 @@ typedef struct {
   int64_t rem_nnz;            /* local remainder non-zeros                    */
   int64_t n_dense_global;     /* tiles over the whole matrix                  */
   int64_t bytes_alg;          /* algorithmic bytes per sable_spmv */
-  int64_t n_groups, n_items;  /* executor work decomposition                  */
   int32_t dtype;
   int32_t delta;
   int32_t suitable;           /* >= 1 dense tile in the matrix */
   int32_t world, rank;
   double inspect_ms;          /* wall time of sable_vbr_create's inspector    */
-  int64_t n_tasks;            /* executor warp tasks (contiguous item ranges) */
-  int32_t exec_grid;          /* CTAs of one sable_spmv launch                */
-  int32_t item_bytes;         /* cap on the bytes one work item streams       */
-  int64_t rem_packets;        /* remainder executor warps (row packets)       */
-  int64_t rem_long_pieces;    /* pieces of remainder rows cut across warps    */
-  int64_t n_chunks;           /* dense executor stage loads (chunks)          */
-  int64_t n_bundles;          /* dense executor lane maps (bundles)           */
-  int64_t stream_bytes;       /* bytes of the dense executor stream           */
-  int64_t n_bundle_lanes;     /* lanes with work summed over the bundles      */
-  /* the unit executor (SABLE_ARCH=2, the default) */
-  int32_t arch;               /* executor of sable_spmv: 2 = units, 1/0 = legacy stream */
-  int32_t unit_staged;        /* 1: units pulled through shared-memory stages  */
+  /* the executor's plan (DESIGN.md sections 5-6) */
+  int32_t exec_grid;          /* CTAs of one sable_spmv launch (one warp each) */
+  int32_t unit_bytes;         /* cap on one unit's bytes                       */
   int64_t n_units;            /* warp work units (<= 32 rows of one block row) */
-  int64_t n_unit_batches;     /* warps of one sable_spmv launch                */
-  int64_t n_combine;          /* row ranges split over several units          */
+  int64_t n_unit_batches;     /* warp batches of consecutive units             */
+  int64_t n_combine;          /* row ranges split over several units           */
   int64_t panel_elems;        /* row-major panel elements (16-byte padded rows) */
-  int64_t xmap_entries;       /* x map entries (one per 16-byte column vector) */
+  int64_t xmap_entries;       /* x map entries (one per 16-byte column vector)  */
 } sable_info;
 
 /* Caller-allocated HOST buffers for sable_export_partition, sized from
@@ -228,20 +218,41 @@ sable_status sable_shard_bounds(const int64_t* weights, int32_t nbrows, int32_t 
  * broadcasts the bytes (e.g. over torch.distributed). */
 sable_status sable_nccl_unique_id(void* out128);
 
-/* Create the handle's NCCL communicator (rank/world from the create shard). */
+/* Create the handle's NCCL communicator (rank/world from the create shard),
+ * its exchange stream, and all-gather every rank's exchange-slice row bounds
+ * (SABLE_E_INVALID_ARG if the ranks' row layouts disagree). */
 sable_status sable_comm_init(sable_handle* h, const void* id128);
 
-/* One exchange step: x_next[row_begin:row_end] = (A x)[local rows], then
- * every rank's slice is all-gathered into x_next (ncols entries) on every
- * rank.  Requires a square matrix (SABLE_E_DIM) and sable_comm_init when
- * world > 1.  x_full and x_next_full are device pointers, not aliased. */
+/* Poll the communicator for an asynchronous NCCL error (non-blocking,
+ * ncclCommGetAsyncError): SABLE_OK, or SABLE_E_NCCL after aborting a failed
+ * communicator.  The exchange calls below poll before enqueueing work. */
+sable_status sable_comm_check(sable_handle* h);
+
+/* One exchange step: x_next[row_begin:row_end] = (A x)[local
+ * rows], then every rank's rows are all-gathered into x_next (ncols entries)
+ * on every rank with in-place ncclBroadcasts.  Pipelined: the shard's rows are
+ * cut into exchange slices of whole row ranges; slice s is broadcast on the
+ * handle's exchange stream while slice s + 1 computes.
+ * Requires a square matrix (SABLE_E_DIM) and sable_comm_init when world > 1.
+ * x_full and x_next_full are device pointers, not aliased.  Asynchronous on
+ * cuda_stream (the exchange stream is forked from and joined back to it). */
 sable_status sable_spmv_allgather(sable_handle* h, const void* x_full, void* x_next_full,
                                   void* cuda_stream);
 
 /* iters exchange steps ping-ponging x_a -> x_b -> x_a ...; *result_in_b = 1
- * if the final x is in x_b.  Asynchronous on cuda_stream. */
+ * if the final x is in x_b.  The steps run as ONE CUDA graph (kernels and
+ * NCCL calls captured once per (x_a, x_b, iters) and relaunched on later
+ * calls) on an internal stream ordered after / before cuda_stream by events.
+ * Asynchronous; bitwise the same as iters sable_spmv_allgather calls. */
 sable_status sable_spmv_iterate(sable_handle* h, void* x_a, void* x_b, int32_t iters,
                                 void* cuda_stream, int32_t* result_in_b);
+
+/* The all-gather layout on the host (no device work): for per-block-row
+ * weights (as in sable_shard_bounds) and the row grid rpntr[nbrows+1], the
+ * global row bounds of every rank's slice of y, row_bounds[world+1]
+ * (row_bounds[q] = rpntr[shard bound q]) -- the rows rank q broadcasts. */
+sable_status sable_exchange_rows(const int64_t* weights, int32_t nbrows, const int32_t* rpntr,
+                                 int32_t world, int64_t* row_bounds);
 
 /* ---- the partitioner ------------------------------
  * Alg. 1 "Matrix Partitioning" on the device: the row
@@ -270,7 +281,7 @@ sable_status sable_partition_grid(int64_t nrows, int64_t ncols, int64_t nnz,
 
 /* ---- multi-vector products ------------------------
  * Y = A X for k right-hand sides in one pass over the inspected matrix (the
- * tile stream and the remainder are read once for all k): Y[:, j] = A X[:, j],
+ * panels and the remainder are read once for all k): Y[:, j] = A X[:, j],
  * y_i = sum_j A_ij x_j per column -- the "user-defined
  * operation" over the same VBR-C split.
  *   X: device, row-major ncols x k (the k values of matrix column c at
@@ -278,17 +289,18 @@ sable_status sable_partition_grid(int64_t nrows, int64_t ncols, int64_t nnz,
  *      (row_end - row_begin) x k, fully written; not aliased with X.
  *   k in {1, 2, 4, 8} (else SABLE_E_UNSUPPORTED).  Asynchronous on
  *   cuda_stream; the first call allocates k-wide scratch (synchronously).
- * Each row's sums run in a fixed order (deterministic run to run), within
- * the SpMV tolerance of the definition, but not bitwise the sable_spmv order.
- * Needs the default CTA-ring executor plan (SABLE_ARCH=1), else
- * SABLE_E_UNSUPPORTED. */
+ * The same unit plan and kernel as sable_spmv with k accumulators per row
+ * (one launch).  Each row's sums run in a fixed order (deterministic run to
+ * run), within the SpMV tolerance of the definition; k = 1 is bitwise
+ * sable_spmv, k > 1 folds lanes in a different fixed tree. */
 sable_status sable_spmm(sable_handle* h, const void* X, void* Y, int32_t k, void* cuda_stream);
 
 /* ---- handle images ---------------------------------
  * Compile once, run many: the inspected state of a handle
- * -- executor stream and plan, remainder CSR and packets, panel values, tile
- * geometry, local cells, scalars incl. the suitability flag of sable_get_info
- * -- as one byte image ("SABLEVC1": header with an FNV-1a
+ * -- the executor's unit plan (units, batches, x maps, combine groups), the
+ * row-major panels, the remainder CSR, tile geometry, local cells, scalars
+ * incl. the suitability flag of sable_get_info -- as one byte
+ * image ("SABLEVC2": header with an FNV-1a
  * checksum, then fixed sections 8-byte aligned).  No NCCL state: call
  * sable_comm_init again on a world > 1 handle.  The image is tied to
  * SABLE_ABI_VERSION and to the executor configuration it was planned with.

@@ -29,6 +29,8 @@ std::string cuda_msg(cudaError_t e, const char* what) {
 sable_status create_impl(const sable_vbr_desc* d, uint32_t delta, const sable_shard* sh,
                          cudaStream_t st, sable_handle** out);
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st);
+cudaError_t run_spmm(const sable_handle* h, const void* X, void* Y, int32_t k, void* scratch,
+                     cudaStream_t st);
 sable_status comm_destroy(sable_handle* h);
 int32_t exec_grid(const sable_handle* h);
 
@@ -46,16 +48,12 @@ cudaError_t set_smem_attr(const void* func, int device, size_t bytes) {
 
 void free_handle(sable_handle* h) {
   if (!h) return;
-  void* dev[] = {h->tval,     h->tiles,      h->xt,       h->rem_ptr,
-                 h->rem_idx,  h->rem_val,    h->scratch,  h->counters,       h->cell_br,
-                 h->cell_bc,  h->cell_cnt,   h->cell_dense, h->tile_canon_off, h->tile_br,
-                 h->br_vbase, h->br_W,       h->xgi,        h->task,       h->cref,       h->stream,     h->x_dev,    h->y_dev,
-                 h->mm_scratch, h->mm_rscratch, h->pv, h->units, h->ubatch, h->xq, h->xside,
-                 h->uxg, h->uscratch, h->ucounters};
+  void* dev[] = {h->rem_ptr,  h->rem_idx,   h->rem_val,    h->pv,          h->units,
+                 h->ubatch,   h->xq,        h->xside,      h->uxg,         h->uscratch,
+                 h->ucounters, h->mm_scratch, h->cell_br,  h->cell_bc,     h->cell_cnt,
+                 h->cell_dense, h->tiles,   h->tile_canon_off, h->tile_br, h->br_pbase,
+                 h->br_W,     h->x_dev,     h->y_dev};
   for (void* p : dev)
-    if (p) cudaFree(p);
-  void* rdev[] = {h->rp.packets, h->rp.scratch, h->rp.counters};
-  for (void* p : rdev)
     if (p) cudaFree(p);
   free(h->all_bounds_h);
   free(h->rpntr_h);
@@ -76,15 +74,16 @@ sable_status cuda_fail(cudaError_t e, const char* what) {
 
 template <typename T>
 __global__ void k_unpack_tiles(const int64_t* canon_off, const TileDesc* desc,
-                               const int32_t* tile_br, const int64_t* br_vbase,
-                               const int32_t* br_W, int32_t br_begin, const T* tval, T* out) {
+                               const int32_t* tile_br, const int64_t* br_pbase,
+                               const int32_t* br_W, int32_t br_begin, const T* pv, T* out) {
   const int64_t t = blockIdx.x;
   const int64_t off = canon_off[t], area = canon_off[t + 1] - off;
   const TileDesc d = desc[t];
   const int64_t h = area / d.w;
   const int32_t la = tile_br[t] - br_begin;
-  for (int64_t e = threadIdx.x; e < area; e += blockDim.x)
-    out[off + e] = tval[panel_pos(br_vbase[la], br_W[la], h, d.cs, e % h, e / h)];
+  const int64_t vec = 16 / (int64_t)sizeof(T);
+  for (int64_t e = threadIdx.x; e < area; e += blockDim.x)  // canonical column-major
+    out[off + e] = pv[panel_rm_pos(br_pbase[la], br_W[la], vec, d.cs, e % h, e / h)];
 }
 
 __global__ void k_not(const uint8_t* in, int64_t n, uint8_t* out) {
@@ -104,8 +103,8 @@ sable_status export_tiles(const sable_handle* h, void* host_out) {
   cudaError_t e = cudaMalloc(&buf, sizeof(T) * h->tile_elems);
   if (e) return cuda_fail(e, "cudaMalloc(export tiles)");
   k_unpack_tiles<T><<<(unsigned)h->n_dense, 128>>>(h->tile_canon_off, h->tiles, h->tile_br,
-                                                  h->br_vbase, h->br_W, h->br_begin,
-                                                  static_cast<const T*>(h->tval), buf);
+                                                  h->br_pbase, h->br_W, h->br_begin,
+                                                  static_cast<const T*>(h->pv), buf);
   e = cudaGetLastError();
   if (!e) e = cudaMemcpy(host_out, buf, sizeof(T) * h->tile_elems, cudaMemcpyDeviceToHost);
   cudaFree(buf);
@@ -195,6 +194,8 @@ sable_status sable_vbr_create(const sable_vbr_desc* d, uint32_t delta_pct,
 sable_status sable_spmv(sable_handle* h, const void* x, void* y, void* cuda_stream) {
   if (!h || !x || (!y && h->row_end > h->row_begin))
     return fail(SABLE_E_INVALID_ARG, "sable_spmv: NULL argument");
+  DeviceGuard g(h->device);
+  if (g.err) return cuda_fail(g.err, "sable_spmv: cudaSetDevice");
   const cudaError_t e = run_spmv(h, x, y, static_cast<cudaStream_t>(cuda_stream));
   return e ? cuda_fail(e, "spmv launch") : SABLE_OK;
 }
@@ -202,6 +203,8 @@ sable_status sable_spmv(sable_handle* h, const void* x, void* y, void* cuda_stre
 sable_status sable_spmv_host(sable_handle* h, const void* x_host, void* y_host,
                              void* cuda_stream) {
   if (!h || !x_host || !y_host) return fail(SABLE_E_INVALID_ARG, "sable_spmv_host: NULL argument");
+  DeviceGuard g(h->device);
+  if (g.err) return cuda_fail(g.err, "sable_spmv_host: cudaSetDevice");
   const size_t sv = h->dtype == SABLE_F64 ? 8 : 4;
   const int64_t nloc = h->row_end - h->row_begin;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
@@ -243,30 +246,19 @@ sable_status sable_get_info(const sable_handle* h, sable_info* info) {
   info->rem_nnz = h->rem_nnz;
   info->n_dense_global = h->n_dense_global;
   info->bytes_alg = h->bytes_alg;
-  info->n_groups = h->n_groups;
-  info->n_items = h->n_items;
   info->dtype = h->dtype;
   info->delta = h->delta;
   info->suitable = h->n_dense_global > 0 ? 1 : 0;
   info->world = h->world;
   info->rank = h->rank;
   info->inspect_ms = h->inspect_ms;
-  info->n_tasks = h->cfg.n_tasks;
   info->exec_grid = exec_grid(h);
-  info->item_bytes = h->cfg.item_bytes;
-  info->rem_packets = h->rp.n_packets;
-  info->rem_long_pieces = h->rp.n_pieces;
-  info->n_chunks = h->n_chunks;
-  info->n_bundles = h->n_bundles;
-  info->stream_bytes = h->stream_bytes;
-  info->n_bundle_lanes = h->n_bundle_lanes;
-  info->arch = h->cfg.arch;
-  info->unit_staged = h->cfg.ustaged;
   info->n_units = h->n_units;
   info->n_unit_batches = h->n_ubatch;
   info->n_combine = h->n_uxg;
   info->panel_elems = h->pv_elems;
   info->xmap_entries = h->n_xq;
+  info->unit_bytes = h->cfg.ustage;
   return SABLE_OK;
 }
 
@@ -328,6 +320,27 @@ sable_status sable_export_partition(const sable_handle* h, const sable_partition
   }
 #undef CP
   return SABLE_OK;
+}
+
+sable_status sable_spmm(sable_handle* h, const void* X, void* Y, int32_t k, void* cuda_stream) {
+  if (!h || !X || (!Y && h->row_end > h->row_begin))
+    return fail(SABLE_E_INVALID_ARG, "sable_spmm: NULL argument");
+  if (k != 1 && k != 2 && k != 4 && k != 8)
+    return fail(SABLE_E_UNSUPPORTED, "sable_spmm: k must be 1, 2, 4 or 8");
+  DeviceGuard g(h->device);
+  if (g.err) return cuda_fail(g.err, "sable_spmm: cudaSetDevice");
+  const size_t sv = h->dtype == SABLE_F64 ? 8 : 4;
+  // k-wide partials of split row ranges: allocated once, for k = 8
+  if (!h->mm_scratch) {
+    const cudaError_t e =
+        cudaMalloc(&h->mm_scratch, sv * 8 * (size_t)std::max<int64_t>(h->uscratch_slots, 1));
+    if (e) {
+      h->mm_scratch = nullptr;
+      return cuda_fail(e, "sable_spmm scratch");
+    }
+  }
+  const cudaError_t e = run_spmm(h, X, Y, k, h->mm_scratch, static_cast<cudaStream_t>(cuda_stream));
+  return e ? cuda_fail(e, "sable_spmm launch") : SABLE_OK;
 }
 
 }  // extern "C"

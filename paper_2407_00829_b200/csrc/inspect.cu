@@ -34,13 +34,13 @@
 
 namespace sable {
 
-cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st);
 void free_handle(sable_handle* h);
 template <typename T>
-cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vector<int32_t>& H_rpntr,
-                       const std::vector<int32_t>& H_W, const std::vector<int64_t>& br_vbase,
-                       const std::vector<int64_t>& br_wprefix, const std::vector<int64_t>& br_t0,
-                       const std::vector<int32_t>& H_rp, const std::vector<XTile>& H_xt,
+cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
+                       const std::vector<int32_t>& H_rpntr, const std::vector<int32_t>& H_W,
+                       const std::vector<int64_t>& br_vbase, const std::vector<int64_t>& br_wprefix,
+                       const std::vector<int64_t>& br_t0, const std::vector<int32_t>& H_rp,
+                       const std::vector<XTile>& H_xt, std::vector<int64_t>& br_pbase,
                        cudaStream_t st);
 
 namespace {
@@ -523,600 +523,24 @@ int64_t env_int(const char* name, int64_t dflt) {
 
 // ------------------------------------------------------------------- a5: plan
 
-int64_t g_lane_work = 48;  // SABLE_LANE_WORK (plan-time tuning; see item_lq)
-
-// Executor shape; SABLE_* environment variables override the defaults
-// (tuning and tests).  Invalid overrides -> SABLE_E_INVALID_ARG.
-ExecCfg exec_config(int sv) {
+// Executor configuration; SABLE_* environment variables override the
+// defaults (tuning runs and tests).  Invalid overrides -> SABLE_E_INVALID_ARG.
+ExecCfg exec_config() {
   ExecCfg c{};
-  c.rem_grid = (int32_t)env_int("SABLE_REM_GRID", 0);
-  c.xpf = (int32_t)env_int("SABLE_XPREFETCH", 1);
-  c.ustaged = (int32_t)env_int("SABLE_UNIT_STAGED", 0);
-  c.arch = (int32_t)env_int("SABLE_ARCH", 2);  // 2: the unit executor (unit.cu)
-  if (c.arch == 1 || c.arch == 2) {
-    // a shared ring per CTA: bigger stages, consumers grab bundles
-    c.nstage = (int32_t)env_int("SABLE_NSTAGE", 4);
-    // default: 3 CTAs per SM (fp32 and fp64) whose stages share the SM's
-    // 228 KB (1 KB reserved per CTA, 256 B of barriers) -- measured r01:
-    // fewer, bigger chunks win (C2 0.054 -> 0.050 ms, C4 0.134 -> 0.113 ms
-    // going from 4 CTAs x 4 x 12 KB to 3 CTAs x 4 x 18.6 KB)
-    const int64_t ctas_dflt = std::min<int64_t>(3, cta_regs_occupancy(sv));
-    const int64_t ctas_env = env_int("SABLE_CTAS_PER_SM", 0);
-    const int64_t fit = ((228 * 1024) / (ctas_env > 0 ? ctas_env : ctas_dflt) - 1024 - 256) /
-                        std::max<int64_t>(1, c.nstage);
-    c.stage_bytes = (int32_t)env_int("SABLE_STAGE_BYTES",
-                                     std::min<int64_t>(65536, fit & ~(int64_t)127));
-    c.item_bytes = (int32_t)env_int("SABLE_ITEM_BYTES", c.stage_bytes - 1024);
-    c.xbuf = 32;
-    const int64_t per_cta = cta_smem_bytes(c, sv);
-    c.ctas_per_sm = (int32_t)(ctas_env > 0 ? ctas_env
-                                           : std::max<int64_t>(1, std::min<int64_t>(
-                                                 ctas_dflt, (227 * 1024) / per_cta)));
-    c.mode = (int32_t)env_int("SABLE_EXEC_MODE", 0);
-    c.n_tasks = (int32_t)env_int("SABLE_TASKS", 0);
-    g_lane_work = std::max<int64_t>(1, env_int("SABLE_LANE_WORK", 48));
-    const bool ok = c.stage_bytes % 128 == 0 && c.stage_bytes >= 1024 && c.stage_bytes <= 65536 &&
-                    c.nstage >= 3 && c.nstage <= kMaxStages && c.item_bytes >= 8 * sv &&
-                    c.item_bytes + 512 <= c.stage_bytes && c.ctas_per_sm >= 1 &&
-                    per_cta * c.ctas_per_sm <= 227 * 1024 && c.n_tasks >= 0;
-    if (!ok) {
-      set_error("invalid SABLE_* executor configuration (arch 1 needs nstage >= 3)");
-      throw Fail{SABLE_E_INVALID_ARG};
-    }
-    return c;  // arch 2 keeps the arch 1 stream for sable_spmm
-  }
-  if (c.arch != 0) {
-    set_error("invalid SABLE_ARCH (0, 1 or 2)");
-    throw Fail{SABLE_E_INVALID_ARG};
-  }
-  // defaults: the best of the r01 sweeps on B200 (C2 / C3 / C4)
-  c.stage_bytes = (int32_t)env_int("SABLE_STAGE_BYTES", 3072);
-  c.nstage = (int32_t)env_int("SABLE_NSTAGE", 2);
-  c.item_bytes = (int32_t)env_int("SABLE_ITEM_BYTES", c.stage_bytes - 512);
-  c.xbuf = (int32_t)env_int("SABLE_XBUF", 384);
-  const int64_t per_cta = (int64_t)kWarps * warp_smem_bytes(c.nstage, c.stage_bytes, c.xbuf, sv);
-  c.ctas_per_sm = (int32_t)env_int(
-      "SABLE_CTAS_PER_SM", std::max<int64_t>(1, std::min<int64_t>(8, (227 * 1024) / per_cta)));
-  c.mode = (int32_t)env_int("SABLE_EXEC_MODE", 0);
-  c.n_tasks = (int32_t)env_int("SABLE_TASKS", 0);  // 0 = one per executor warp
-  g_lane_work = std::max<int64_t>(1, env_int("SABLE_LANE_WORK", 48));
-  const bool ok = c.stage_bytes % 128 == 0 && c.stage_bytes >= 1024 && c.stage_bytes <= 65536 &&
-                  c.nstage >= 2 && c.nstage <= kMaxStages && c.item_bytes >= 8 * sv &&
-                  c.item_bytes + 512 <= c.stage_bytes && c.xbuf >= 32 && c.xbuf <= 32768 &&
-                  c.ctas_per_sm >= 1 && per_cta * c.ctas_per_sm <= 227 * 1024 && c.n_tasks >= 0;
-  if (!ok) {
-    set_error("invalid SABLE_STAGE_BYTES / SABLE_NSTAGE / SABLE_ITEM_BYTES / SABLE_XBUF / "
-              "SABLE_CTAS_PER_SM / SABLE_TASKS combination");
+  c.pf = (int32_t)env_int("SABLE_XPREFETCH", 1);
+  c.ustage = (int32_t)env_int("SABLE_USTAGE", kUnitBytes);
+  c.rem_rows = (int32_t)env_int("SABLE_UREM_ROWS", 32);
+  c.batch = (int32_t)env_int("SABLE_UBATCH_UNITS", kUnitBatch);
+  c.sliced = env_int("SABLE_SLICED", 0) != 0 ? 1 : 0;
+  const int64_t arch = env_int("SABLE_ARCH", 2);
+  if (arch != 2 || c.ustage < 1024 || c.ustage % 16 != 0 || c.ustage > (1 << 24) ||
+      c.rem_rows < 1 || c.rem_rows > 32 || c.batch < 1 || (c.pf != 0 && c.pf != 1)) {
+    set_error("invalid SABLE_ARCH / SABLE_USTAGE / SABLE_UREM_ROWS / SABLE_UBATCH_UNITS / "
+              "SABLE_XPREFETCH (arch 2 only; ustage a multiple of 16 in [1024, 2^24]; "
+              "1..32 rows; batch >= 1)");
     throw Fail{SABLE_E_INVALID_ARG};
   }
   return c;
-}
-
-int device_sms() {
-  int dev = 0, n = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 148;
-}
-
-// Per chunk, for the stream packer.
-struct PackDesc {
-  int64_t soff;      // stream offset of the chunk
-  int64_t meta_src;  // offset of its metadata image in the upload buffer
-  int64_t v_lo;      // first dense value
-  int32_t meta_bytes, o_rptr, o_val, o_ridx, o_rval;
-  int32_t nv, r_lo, nrow1, e_lo, nent;
-};
-
-// One CTA per chunk: metadata image, row pointers, values, remainder.
-template <typename T>
-__global__ void k_pack_stream(const PackDesc* pd, const unsigned char* meta, const int32_t* rem_ptr,
-                              const T* tval, const int32_t* ridx, const T* rval,
-                              unsigned char* stream) {
-  const PackDesc d = pd[blockIdx.x];
-  unsigned char* dst = stream + d.soff;
-  const uint32_t* ms = reinterpret_cast<const uint32_t*>(meta + d.meta_src);
-  uint32_t* md = reinterpret_cast<uint32_t*>(dst);
-  for (int i = threadIdx.x; i < d.meta_bytes / 4; i += blockDim.x) md[i] = ms[i];
-  int32_t* rp = reinterpret_cast<int32_t*>(dst + d.o_rptr);
-  for (int i = threadIdx.x; i < d.nrow1; i += blockDim.x) rp[i] = rem_ptr[d.r_lo + i];
-  T* vv = reinterpret_cast<T*>(dst + d.o_val);
-  for (int i = threadIdx.x; i < d.nv; i += blockDim.x) vv[i] = tval[d.v_lo + i];
-  int32_t* ri = reinterpret_cast<int32_t*>(dst + d.o_ridx);
-  T* rv = reinterpret_cast<T*>(dst + d.o_rval);
-  for (int i = threadIdx.x; i < d.nent; i += blockDim.x) {
-    ri[i] = ridx[d.e_lo + i];
-    rv[i] = rval[d.e_lo + i];
-  }
-}
-
-inline int64_t al16(int64_t v) { return (v + 15) & ~(int64_t)15; }
-
-// Plan-time work item.
-struct HItem {
-  int64_t voff, eb, xp;
-  int32_t ne, ncol, row0, nr, maxrow, nseg;
-  int32_t g, p, np;
-  uint8_t flags;
-};
-
-// Bundle lane maps.  Item i gets Q_i = 2^lq_i phases: the smallest power of
-// two with ceil(w_i / Q_i) <= lane work (w_i = its columns + its longest
-// remainder row) and nr_i * Q_i <= 32.  Q_i depends on the item alone, so a
-// row's summation order never depends on how items are packed into bundles
-// (or on the shard); bundles only pack items with sum_i nr_i * Q_i <= 32.
-
-struct BundleState {
-  std::vector<int> nr, lq;
-  int lanes = 0;
-  int64_t maxw = 0;
-  bool single = false;  // a split-group piece: alone, lane = ph * nr + r
-};
-
-int item_lq(int nr, int64_t w) {
-  int lq = 0;
-  while (((w + (1ll << lq) - 1) >> lq) > g_lane_work && (nr << (lq + 1)) <= 32) ++lq;
-  return lq;
-}
-
-constexpr int64_t kBundleOverhead = 8;  // fixed cost of a bundle, in lane-steps
-
-// Work items (row groups or pieces of groups larger than a stage), chunks
-// (one stage each), bundles (lane maps) and warp tasks (contiguous chunk
-// ranges of about equal bytes), then the packed executor stream.  Items
-// depend only on the block rows and a group's pieces are summed left to
-// right whoever processes them, so y is identical for every shard count.
-template <typename T>
-void plan_executor(sable_handle* h, ExecCfg& cfg, int32_t nbl, int32_t b0,
-                   const std::vector<int32_t>& H_rpntr, const std::vector<int32_t>& H_W,
-                   const std::vector<int64_t>& br_vbase, const std::vector<int64_t>& br_wprefix,
-                   const std::vector<int32_t>& H_rp, const std::vector<XTile>& H_tile,
-                   cudaStream_t st) {
-  const int64_t sv = sizeof(T);
-  const int64_t cap = cfg.item_bytes;
-
-  // runs: adjacent tiles whose flattened and global columns advance together
-  std::vector<XTile> R;
-  const int64_t ntile = (int64_t)H_tile.size() - 1;
-  for (int64_t t = 0; t < ntile; ++t) {
-    if (!R.empty() && (int64_t)H_tile[t].c0 - H_tile[t].tp == (int64_t)R.back().c0 - R.back().tp)
-      continue;
-    R.push_back(H_tile[t]);
-  }
-  const int64_t nrun = (int64_t)R.size();
-  R.push_back(XTile{ntile > 0 ? H_tile[ntile].tp : 0, 0});  // sentinel
-  auto run_of = [&](int64_t pc) {  // last run with tp <= pc
-    return (int64_t)(std::upper_bound(R.begin(), R.begin() + nrun, pc,
-                                      [](int64_t v, const XTile& t) { return v < (int64_t)t.tp; }) -
-                     R.begin() - 1);
-  };
-  auto nseg_of = [&](int64_t xp, int64_t ncol) -> int32_t {
-    if (ncol <= 0) return 0;
-    return (int32_t)(run_of(xp + ncol - 1) - run_of(xp) + 1);
-  };
-  auto maxrow_of = [&](int32_t row0, int nr, int64_t e0, int64_t e1) {
-    int32_t m = 0;
-    for (int r = 0; r < nr; ++r) {
-      const int64_t lo = std::max<int64_t>(H_rp[row0 + r], e0), hi = std::min<int64_t>(H_rp[row0 + r + 1], e1);
-      m = std::max<int32_t>(m, (int32_t)std::max<int64_t>(0, hi - lo));
-    }
-    return m;
-  };
-
-  // ---- items
-  std::vector<HItem> It;
-  It.reserve((size_t)(H_rp.size() / 8 + nbl + 1));
-  int64_t slot = 0, ngroups = 0;
-  const int64_t xcap = 32767;  // item columns are 16-bit
-  for (int32_t la = 0; la < nbl; ++la) {
-    const int32_t a = b0 + la;
-    const int32_t hgt = H_rpntr[a + 1] - H_rpntr[a];
-    const int64_t W = H_W[a];
-    const int32_t r0 = (int32_t)(H_rpntr[a] - h->row_begin);
-    const int64_t xp = br_wprefix[la];
-    for (int32_t j = 0; j * kGroupRows < hgt; ++j) {
-      HItem base{};
-      base.row0 = r0 + j * kGroupRows;
-      base.nr = std::min(kGroupRows, hgt - j * kGroupRows);
-      base.g = (int32_t)ngroups;
-      const int64_t voff = br_vbase[la] + (int64_t)j * kGroupRows * W;
-      // the remainder has its own executor (rem.cu): items carry dense work
-      // only, and block rows without tiles have no items
-      if (W == 0) continue;
-      const int64_t eb = H_rp[base.row0], ee = eb;
-      const int64_t meta = 16 + 8 + 4 * (base.nr + 1) + 8 * nseg_of(xp, W);
-      const int64_t bytes = W * base.nr * sv + (ee - eb) * (sv + 4) + meta;
-      const size_t first = It.size();
-      if (bytes <= cap && W + (ee - eb) <= xcap && ee - eb <= 65535) {
-        HItem it = base;
-        it.voff = voff;
-        it.eb = eb;
-        it.ne = (int32_t)(ee - eb);
-        it.ncol = (int32_t)W;
-        it.xp = xp;
-        It.push_back(it);
-      } else {
-        // pieces: column ranges (each <= cap bytes incl. its x segments), then entry ranges
-        int64_t c = 0;
-        while (c < W) {
-          int64_t n = std::max<int64_t>(1, std::min<int64_t>(xcap, (cap - 64) / (base.nr * sv + 8)));
-          n = std::min(n, W - c);
-          HItem it = base;
-          it.voff = voff + c * base.nr;
-          it.eb = ee;
-          it.ncol = (int32_t)n;
-          it.xp = xp + c;
-          It.push_back(it);
-          c += n;
-        }
-        const int64_t rc = std::max<int64_t>(1, std::min<int64_t>(xcap, (cap - 64 - 4 * (base.nr + 1)) / (sv + 4)));
-        for (int64_t e = eb; e < ee; e += rc) {
-          HItem it = base;
-          it.voff = voff;
-          it.eb = e;
-          it.ne = (int32_t)(std::min(ee, e + rc) - e);
-          It.push_back(it);
-        }
-        if (It.size() == first) It.push_back(base);
-      }
-      const int32_t np = (int32_t)(It.size() - first);
-      for (size_t q = first; q < It.size(); ++q) {
-        HItem& it = It[q];
-        it.flags = (uint8_t)((q == first ? IF_FIRST : 0) | (q + 1 == It.size() ? IF_LAST : 0));
-        it.p = (int32_t)(q - first);
-        it.np = np;
-        it.nseg = nseg_of(it.xp, it.ncol);
-        it.maxrow = it.ne > 0 ? maxrow_of(it.row0, it.nr, it.eb, it.eb + it.ne) : 0;
-      }
-      if (np > 1) slot += (int64_t)np * kGroupRows;
-      ++ngroups;
-    }
-  }
-  const int64_t nit = (int64_t)It.size();
-
-  // ---- chunks (greedy: consecutive items that fit a stage) with bundles
-  struct CAcc {
-    int64_t i0 = 0, ni = 0, vlo = 0, vhi = 0, elo = 0, ehi = 0, rlo = 0, rhi = 0;
-    int64_t ndx = 0, ng = 0;
-    bool dv = false, de = false;
-    std::vector<BundleState> B;
-    std::vector<int64_t> bitem;  // first item (chunk-relative) of each bundle
-  };
-  auto chunk_bytes = [&](const CAcc& A) {
-    const int64_t o_rptr = al16(64 + 16 * A.ni + 128 * (int64_t)A.B.size() + 8 * A.ng);
-    const int64_t nent = A.de ? A.ehi - A.elo : 0;
-    return o_rptr + al16(4 * (A.de ? A.rhi - A.rlo + 1 : 0)) + al16(sv * (A.dv ? A.vhi - A.vlo : 0)) +
-           al16(4 * nent) + al16(sv * nent);
-  };
-  auto fits = [&](const CAcc& A) {
-    const int64_t nent = A.de ? A.ehi - A.elo : 0;
-    return chunk_bytes(A) <= cfg.stage_bytes && A.ni <= 255 && nent <= 65535;
-  };
-  auto add_item = [&](CAcc A, int64_t i) {
-    const HItem& it = It[i];
-    if (A.ni == 0) A.i0 = i;
-    const int64_t rel = A.ni;
-    A.ni++;
-    A.ndx += it.ncol;
-    A.ng += it.nseg;
-    if (it.ncol > 0) {
-      const int64_t v0 = it.voff, v1 = it.voff + (int64_t)it.ncol * it.nr;
-      if (!A.dv) { A.vlo = v0; A.vhi = v1; A.dv = true; }
-      else { A.vlo = std::min(A.vlo, v0); A.vhi = std::max(A.vhi, v1); }
-    }
-    if (it.ne > 0) {
-      const int64_t e0 = it.eb, e1 = it.eb + it.ne;
-      if (!A.de) { A.elo = e0; A.ehi = e1; A.rlo = it.row0; A.rhi = it.row0 + it.nr; A.de = true; }
-      else {
-        A.elo = std::min(A.elo, e0); A.ehi = std::max(A.ehi, e1);
-        A.rlo = std::min<int64_t>(A.rlo, it.row0); A.rhi = std::max<int64_t>(A.rhi, it.row0 + it.nr);
-      }
-    }
-    // bundle: split-group pieces alone (canonical map); otherwise join the
-    // open bundle if its lanes allow and the lanes' work does not grow much
-    const int64_t w = (int64_t)it.ncol + it.maxrow;
-    const bool single = it.np > 1;
-    int lq = item_lq(it.nr, w);
-    if (single)  // canonical map: Q = 32 / nr phases, lane = ph * nr + r
-      while ((it.nr << (lq + 1)) <= 32) ++lq;
-    const int64_t wl = (w + (1ll << lq) - 1) >> lq;
-    bool merged = false;
-    if (!single && !A.B.empty() && !A.B.back().single) {
-      BundleState& M = A.B.back();
-      if (M.lanes + (it.nr << lq) <= 32 && wl <= 2 * M.maxw + kBundleOverhead &&
-          M.maxw <= 2 * wl + kBundleOverhead) {
-        M.nr.push_back(it.nr);
-        M.lq.push_back(lq);
-        M.lanes += it.nr << lq;
-        M.maxw = std::max(M.maxw, wl);
-        merged = true;
-      }
-    }
-    if (!merged) {
-      BundleState S1;
-      S1.nr = {it.nr};
-      S1.lq = {lq};
-      S1.lanes = it.nr << lq;
-      S1.maxw = wl;
-      S1.single = single;
-      A.B.push_back(S1);
-      A.bitem.push_back(rel);
-    }
-    return A;
-  };
-
-  std::vector<CAcc> Ch;
-  {
-    CAcc cur;
-    for (int64_t i = 0; i < nit; ++i) {
-      CAcc nxt = add_item(cur, i);
-      if (cur.ni > 0 && !fits(nxt)) {
-        Ch.push_back(std::move(cur));
-        nxt = add_item(CAcc{}, i);
-      }
-      if (!fits(nxt)) {
-        set_error("internal: a work item does not fit one executor stage");
-        throw Fail{SABLE_E_UNSUPPORTED};
-      }
-      cur = std::move(nxt);
-    }
-    if (cur.ni > 0) Ch.push_back(std::move(cur));
-  }
-  const int64_t nch = (int64_t)Ch.size();
-
-  // ---- warp tasks: contiguous chunk ranges of about equal bytes; a cut moves
-  // to the next group boundary when one is near, so only groups larger than a
-  // fraction of a task are shared between warps (and combined in scratch)
-  const int64_t grid = (int64_t)device_sms() * cfg.ctas_per_sm;
-  const int64_t per_task = cfg.arch == 1 ? 1 : kWarps;  // arch 1: a task per CTA
-  const int64_t ntask = cfg.n_tasks > 0 ? cfg.n_tasks : std::max<int64_t>(1, grid * per_task);
-  cfg.n_tasks = (int32_t)ntask;
-  std::vector<int64_t> cbytes(nch), cpre(nch + 1, 0);
-  for (int64_t k = 0; k < nch; ++k) {
-    cbytes[k] = (chunk_bytes(Ch[k]) + 127) & ~(int64_t)127;
-    cpre[k + 1] = cpre[k] + cbytes[k];
-  }
-  std::vector<int32_t> task(ntask + 1, 0);
-  auto starts_group = [&](int64_t k) { return (It[Ch[k].i0].flags & IF_FIRST) != 0; };
-  {
-    int64_t k = 0;
-    const int64_t slack = std::max<int64_t>(1, (cpre[nch] / ntask) / 4);
-    for (int64_t t = 1; t < ntask; ++t) {
-      const int64_t target = cpre[nch] * t / ntask;
-      while (k < nch && cpre[k] < target) ++k;
-      int64_t kk = k;  // boundary before chunk kk: prefer one that starts a group
-      while (kk < nch && !starts_group(kk) && cpre[kk] - target < slack) ++kk;
-      if (kk < nch && !starts_group(kk)) kk = k;
-      k = std::max<int64_t>(kk, task[t - 1]);
-      task[t] = (int32_t)k;
-    }
-    task[ntask] = (int32_t)nch;
-  }
-  if (cfg.arch == 1)  // bundles go to any warp of the CTA: split groups meet in scratch
-    for (auto& it : It)
-      if (it.np > 1) it.flags |= IF_XG;
-  for (int64_t t = 1; t < ntask; ++t) {  // groups cut by a task boundary
-    const int64_t k = task[t];
-    if (k <= 0 || k >= nch) continue;
-    int64_t g0 = Ch[k].i0;
-    if (It[g0].flags & IF_FIRST) continue;
-    while (!(It[g0].flags & IF_FIRST)) --g0;
-    for (int64_t q = g0; q < g0 + It[g0].np; ++q) It[q].flags |= IF_XG;
-  }
-  std::vector<int32_t> task_of(nch, 0);
-  for (int64_t t = 0; t < ntask; ++t)
-    for (int64_t k = task[t]; k < task[t + 1]; ++k) task_of[k] = (int32_t)t;
-
-  // ---- metadata images and pack descriptors
-  std::vector<ChunkRef> cref(nch);
-  for (int64_t k = 0; k < nch; ++k) cref[k] = ChunkRef{cpre[k], (int32_t)chunk_bytes(Ch[k]), 0};
-  std::vector<unsigned char> meta;
-  std::vector<PackDesc> pd(nch);
-  std::vector<XgInfo> Xg(nit);
-  for (int64_t k = 0; k < nch; ++k) {
-    const CAcc& A = Ch[k];
-    const int64_t nb = (int64_t)A.B.size();
-    ChunkHdr hd{};
-    const int64_t kn = k + cfg.nstage;
-    hd.next = (kn < nch && task_of[kn] == task_of[k]) ? cref[kn] : ChunkRef{0, 0, 0};
-    hd.o_item = 64;
-    hd.o_lane = (uint16_t)(64 + 16 * A.ni);
-    hd.o_gath = (uint16_t)(hd.o_lane + 128 * nb);
-    hd.o_rptr = (uint16_t)al16(hd.o_gath + 8 * A.ng);
-    const int64_t nrow1 = A.de ? A.rhi - A.rlo + 1 : 0, nv = A.dv ? A.vhi - A.vlo : 0;
-    const int64_t nent = A.de ? A.ehi - A.elo : 0;
-    hd.o_val = (uint16_t)(hd.o_rptr + al16(4 * nrow1));
-    hd.o_ridx = (uint16_t)(hd.o_val + al16(sv * nv));
-    hd.o_rval = (uint16_t)(hd.o_ridx + al16(4 * nent));
-    hd.ni = (uint16_t)A.ni;
-    hd.nb = (uint16_t)nb;
-    hd.ng = (uint16_t)A.ng;
-    hd.ndx = 0;
-    hd.r0 = (int32_t)A.rlo;
-    hd.e0 = (int32_t)A.elo;
-    hd.nent = (int32_t)nent;
-    hd.i0 = (int32_t)A.i0;
-    const size_t mstart = meta.size();
-    meta.resize(mstart + hd.o_rptr, 0);
-    unsigned char* m = meta.data() + mstart;
-    memcpy(m, &hd, sizeof(hd));
-    SItem* si = reinterpret_cast<SItem*>(m + hd.o_item);
-    XRun* xr = reinterpret_cast<XRun*>(m + hd.o_gath);
-    int64_t gi = 0;
-    for (int64_t q = 0; q < A.ni; ++q) {
-      const HItem& it = It[A.i0 + q];
-      SItem s{};
-      s.v = (uint16_t)(it.ncol > 0 ? it.voff - A.vlo : 0);
-      s.e = (uint16_t)(it.ne > 0 ? it.eb - A.elo : 0);
-      s.ne = (uint16_t)it.ne;
-      s.ncol = (uint16_t)it.ncol;
-      s.row0 = it.row0;
-      s.xb = (uint16_t)gi;
-      s.nr = (uint8_t)it.nr;
-      s.flags = it.flags;
-      si[q] = s;
-      // x runs: the runs under the item's columns
-      for (int64_t c = 0; c < it.ncol;) {
-        const int64_t r = run_of(it.xp + c);
-        const int64_t end = std::min<int64_t>(it.ncol, (int64_t)R[r + 1].tp - it.xp);
-        xr[gi++] = XRun{(int32_t)(R[r].c0 - R[r].tp + it.xp), (uint16_t)c, (uint16_t)end};
-        c = end;
-      }
-    }
-    // lane maps
-    uint32_t* lm = reinterpret_cast<uint32_t*>(m + hd.o_lane);
-    for (int64_t b = 0; b < nb; ++b) {
-      const BundleState& Bs = A.B[b];
-      int lane = 0;
-      for (size_t q = 0; q < Bs.nr.size(); ++q) {
-        const int item = (int)(A.bitem[b] + q), nr = Bs.nr[q], lq = Bs.lq[q];
-        for (int ph = 0; ph < (1 << lq); ++ph)
-          for (int r = 0; r < nr; ++r)
-            lm[b * 32 + lane++] = (uint32_t)item | (uint32_t)r << 8 | (uint32_t)ph << 13 |
-                                  (uint32_t)lq << 18 | kLaneValid;
-      }
-      for (; lane < 32; ++lane) lm[b * 32 + lane] = 0;
-    }
-    PackDesc d{};
-    d.soff = cpre[k];
-    d.meta_src = (int64_t)mstart;
-    d.v_lo = A.vlo;
-    d.meta_bytes = hd.o_rptr;
-    d.o_rptr = hd.o_rptr;
-    d.o_val = hd.o_val;
-    d.o_ridx = hd.o_ridx;
-    d.o_rval = hd.o_rval;
-    d.nv = (int32_t)nv;
-    d.r_lo = (int32_t)A.rlo;
-    d.nrow1 = (int32_t)nrow1;
-    d.e_lo = (int32_t)A.elo;
-    d.nent = (int32_t)nent;
-    pd[k] = d;
-  }
-  // cross-task combine slots (group scratch bases)
-  {
-    int64_t sl = 0;
-    for (int64_t i = 0; i < nit;) {
-      const int64_t np = It[i].np;
-      for (int64_t q = i; q < i + np; ++q) {
-        Xg[q].slot = np > 1 ? sl : 0;
-        Xg[q].g = It[q].g;
-        Xg[q].p = It[q].p;
-        Xg[q].npieces = (int32_t)np;
-      }
-      if (np > 1) sl += np * kGroupRows;
-      i += np;
-    }
-  }
-
-  // ---- upload and pack
-  h->n_groups = ngroups;
-  h->n_items = nit;
-  h->n_chunks = nch;
-  h->n_runs = nrun;
-  h->n_bundles = 0;
-  h->n_bundle_lanes = 0;
-  for (const auto& c : Ch) {
-    h->n_bundles += (int64_t)c.B.size();
-    for (const auto& b : c.B)
-      for (size_t q = 0; q < b.nr.size(); ++q) h->n_bundle_lanes += (int64_t)b.nr[q] << b.lq[q];
-  }
-  h->stream_bytes = cpre[nch];
-  h->stream = dev_alloc<unsigned char>(cpre[nch], st);
-  h->cref = dev_alloc<ChunkRef>(nch, st);
-  h->xgi = dev_alloc<XgInfo>(nit, st);
-  h->task = dev_alloc<int32_t>(ntask + 1, st);
-  if (nch) {
-    SB_CU(cudaMemcpyAsync(h->cref, cref.data(), sizeof(ChunkRef) * nch, cudaMemcpyHostToDevice, st));
-    DevBuf mb, pb;
-    SB_CU(mb.alloc(meta.size(), st));
-    SB_CU(pb.alloc(sizeof(PackDesc) * nch, st));
-    SB_CU(cudaMemcpyAsync(mb.p, meta.data(), meta.size(), cudaMemcpyHostToDevice, st));
-    SB_CU(cudaMemcpyAsync(pb.p, pd.data(), sizeof(PackDesc) * nch, cudaMemcpyHostToDevice, st));
-    k_pack_stream<T><<<(unsigned)nch, 256, 0, st>>>(pb.as<PackDesc>(), mb.as<unsigned char>(),
-                                                    h->rem_ptr, static_cast<const T*>(h->tval),
-                                                    h->rem_idx, static_cast<const T*>(h->rem_val),
-                                                    h->stream);
-    SB_CU(cudaGetLastError());
-    SB_CU(cudaStreamSynchronize(st));
-  }
-  if (nit)
-    SB_CU(cudaMemcpyAsync(h->xgi, Xg.data(), sizeof(XgInfo) * nit, cudaMemcpyHostToDevice, st));
-  SB_CU(cudaMemcpyAsync(h->task, task.data(), sizeof(int32_t) * (ntask + 1), cudaMemcpyHostToDevice, st));
-  h->scratch_elems = slot;
-  h->scratch = dev_alloc<T>(slot, st);
-  h->counters = dev_alloc<int32_t>(ngroups, st);
-  SB_CU(cudaMemsetAsync(h->counters, 0, sizeof(int32_t) * std::max<int64_t>(ngroups, 1), st));
-  SB_CU(cudaStreamSynchronize(st));  // host temporaries
-  cudaFree(h->xt);  // the per-tile map was only needed to plan
-  h->xt = nullptr;
-}
-
-// The remainder executor's plan: packets of whole consecutive rows with up to
-// kPacketEntries entries and kPacketRows rows (every local row is in one, so
-// the executor writes every row); a row longer than kPieceLen is cut into
-// warp pieces of kPieceLen entries, summed in order by the last to arrive.
-template <typename T>
-void plan_remainder(sable_handle* h, const std::vector<int32_t>& H_rp, cudaStream_t st) {
-  const int64_t nloc = (int64_t)H_rp.size() - 1;
-  // packet shape (SABLE_REM_ENTRIES / SABLE_REM_ROWS: tuning, <= the shared
-  // buffers of rem_kernel); a row longer than a packet is cut into pieces
-  const int64_t kPE = env_int("SABLE_REM_ENTRIES", kPacketEntries);
-  const int64_t kPR = env_int("SABLE_REM_ROWS", kPacketRows);
-  if (kPE < 32 || kPE > kPacketEntries || kPR < 1 || kPR > kPacketRows) {
-    set_error("invalid SABLE_REM_ENTRIES / SABLE_REM_ROWS");
-    throw Fail{SABLE_E_INVALID_ARG};
-  }
-  const int64_t kPL = std::min<int64_t>(kPieceLen, kPE);
-  std::vector<RemPacket> pk;
-  int64_t slot = 0, nlong = 0;
-  int64_t r = 0;
-  while (r < nloc) {
-    const int64_t len = (int64_t)H_rp[r + 1] - H_rp[r];
-    if (len > kPL) {
-      const int32_t np = (int32_t)((len + kPL - 1) / kPL);
-      for (int32_t q = 0; q < np; ++q) {
-        RemPacket p{};
-        p.r0 = (int32_t)r;
-        p.r1 = -1 - q;
-        p.e0 = (int32_t)(H_rp[r] + (int64_t)q * kPL);
-        p.e1 = (int32_t)std::min<int64_t>(H_rp[r + 1], (int64_t)p.e0 + kPL);
-        p.npieces = np;
-        p.slot = (int32_t)slot;
-        p.counter = (int32_t)nlong;
-        pk.push_back(p);
-      }
-      slot += np;
-      ++nlong;
-      ++r;
-      continue;
-    }
-    RemPacket p{};
-    p.r0 = (int32_t)r;
-    p.e0 = H_rp[r];
-    int64_t r1 = r;
-    while (r1 < nloc && r1 - r < kPR) {
-      const int64_t l1 = (int64_t)H_rp[r1 + 1] - H_rp[r1];
-      if (l1 > kPL) break;
-      if (r1 > r && (int64_t)H_rp[r1 + 1] - H_rp[r] > kPE) break;
-      ++r1;
-    }
-    p.r1 = (int32_t)r1;
-    p.e1 = H_rp[r1];
-    pk.push_back(p);
-    r = r1;
-  }
-  RemHost& R = h->rp;
-  R.n_packets = (int64_t)pk.size();
-  R.n_pieces = slot;
-  R.n_long = nlong;
-  R.packets = dev_alloc<RemPacket>(R.n_packets, st);
-  R.scratch = dev_alloc<T>(slot, st);
-  R.counters = dev_alloc<int32_t>(nlong, st);
-  SB_CU(cudaMemsetAsync(R.counters, 0, sizeof(int32_t) * std::max<int64_t>(nlong, 1), st));
-  if (R.n_packets)
-    SB_CU(cudaMemcpyAsync(R.packets, pk.data(), sizeof(RemPacket) * pk.size(), cudaMemcpyHostToDevice, st));
-  SB_CU(cudaStreamSynchronize(st));
 }
 
 // ------------------------------------------------------------------- inspect
@@ -1359,12 +783,16 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
   }
   h->tile_br = dev_alloc<int32_t>(n_dense, st);
   h->tiles = dev_alloc<TileDesc>(n_dense, st);
-  h->xt = dev_alloc<XTile>(n_dense + 1, st);
-  SB_CU(cudaMemsetAsync(h->xt, 0, sizeof(XTile) * (n_dense + 1), st));
+  DevBuf xt_b;  // plan-time map of the tiles' columns
+  SB_CU(xt_b.alloc(sizeof(XTile) * (n_dense + 1), st));
+  XTile* xt = xt_b.as<XTile>();
+  SB_CU(cudaMemsetAsync(xt, 0, sizeof(XTile) * (n_dense + 1), st));
   h->tile_canon_off = dev_alloc<int64_t>(n_dense + 1, st);
-  h->br_vbase = dev_alloc<int64_t>(nbl + 1, st);
+  DevBuf vbase_b;
+  SB_CU(vbase_b.alloc(sizeof(int64_t) * (nbl + 1), st));
+  int64_t* d_vbase = vbase_b.as<int64_t>();
   h->br_W = dev_alloc<int32_t>(nbl + 1, st);
-  SB_CU(cudaMemcpyAsync(h->br_vbase, br_vbase.data(), sizeof(int64_t) * (nbl + 1), cudaMemcpyHostToDevice, st));
+  SB_CU(cudaMemcpyAsync(d_vbase, br_vbase.data(), sizeof(int64_t) * (nbl + 1), cudaMemcpyHostToDevice, st));
   std::vector<int32_t> Wloc(nbl + 1, 0);
   for (int32_t la = 0; la < nbl; ++la) Wloc[la] = H_W[b0 + la];
   SB_CU(cudaMemcpyAsync(h->br_W, Wloc.data(), sizeof(int32_t) * (nbl + 1), cudaMemcpyHostToDevice, st));
@@ -1388,20 +816,22 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
     cub_run([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, tw64, ws, n_dense, st); }, st);
     k_tile_desc<<<nblocks_for(n_dense, TH), TH, 0, st>>>(tile_cell, n_dense, cell_bc, h->tile_br,
                                                          tw, ws, wpre_b.as<int64_t>(), b0,
-                                                         in.cpntr, h->tiles, h->xt);
+                                                         in.cpntr, h->tiles, xt);
   }
-  h->tval = dev_alloc<T>(tile_elems, st);
-  SB_CU(cudaMemsetAsync(h->tval, 0, sizeof(T) * std::max<int64_t>(tile_elems, 1), st));
+  // staging slabs of the dense tiles (row groups, column-major), repacked
+  // into the executor's row-major panels by plan_units and then freed
+  DevBuf tval_b;
+  SB_CU(tval_b.alloc(sizeof(T) * std::max<int64_t>(tile_elems, 1), st));
+  T* tval = tval_b.as<T>();
+  SB_CU(cudaMemsetAsync(tval, 0, sizeof(T) * std::max<int64_t>(tile_elems, 1), st));
   if (n_dense > 0)
     k_pack_vbr<T><<<(unsigned)n_dense, 128, 0, st>>>(tile_cell, n_dense, cell_blk, h->tile_br,
                                                       h->tiles, in.rpntr, in.indx, val,
-                                                      h->br_vbase, h->br_W, b0,
-                                                      static_cast<T*>(h->tval));
+                                                      d_vbase, h->br_W, b0, tval);
   if (n_dense > 0 && R > 0)
     k_pack_rem<T><<<nblocks_for(R, TH), TH, 0, st>>>(rowid, in.ridx, rval, R, ecell, cell_lo,
                                                      cell_hi, cell_tile, h->tile_br, h->tiles,
-                                                     in.rpntr, h->br_vbase, h->br_W, b0,
-                                                     static_cast<T*>(h->tval));
+                                                     in.rpntr, d_vbase, h->br_W, b0, tval);
   SB_CU(cudaGetLastError());
 
   // ---- a4: the local CSR remainder ------------------------------------------------
@@ -1517,14 +947,15 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
   std::vector<int32_t> H_rp(nloc + 1);
   d2h(H_rp.data(), h->rem_ptr, nloc + 1, st);
   std::vector<XTile> H_xt(n_dense + 1);
-  d2h(H_xt.data(), h->xt, n_dense + 1, st);
+  d2h(H_xt.data(), xt, n_dense + 1, st);
   SB_CU(cudaStreamSynchronize(st));
-  ExecCfg cfg = exec_config((int)sv);
-  plan_executor<T>(h, cfg, nbl, b0, H_rpntr, H_W, br_vbase, br_wprefix, H_rp, H_xt, st);
-  h->cfg = cfg;
-  plan_remainder<T>(h, H_rp, st);
-  if (cfg.arch == 2) SB_CU(plan_units<T>(h, nbl, b0, H_rpntr, H_W, br_vbase, br_wprefix, br_t0,
-                                         H_rp, H_xt, st));
+  h->cfg = exec_config();
+  std::vector<int64_t> br_pbase;
+  SB_CU(plan_units<T>(h, tval, nbl, b0, H_rpntr, H_W, br_vbase, br_wprefix, br_t0, H_rp, H_xt,
+                      br_pbase, st));
+  h->br_pbase = dev_alloc<int64_t>(nbl + 1, st);
+  SB_CU(cudaMemcpyAsync(h->br_pbase, br_pbase.data(), sizeof(int64_t) * (nbl + 1),
+                        cudaMemcpyHostToDevice, st));
 
   // ---- bookkeeping ---------------------------------------------------------------------
   int64_t nnz = 0;

@@ -8,9 +8,9 @@
 // (PAPER.md:747): a unit never crosses a block row that has dense tiles.
 //
 // Every unit's data (dense rows, x map, remainder row pointers, columns and
-// values, each as its 16-byte-aligned cover) fits one shared-memory stage of
-// the executor (UnitBudget::stage), so the executor can pull a whole unit in
-// with bulk copies while it computes the previous one.
+// values, each as its 16-byte-aligned cover) is capped at UnitBudget::stage
+// bytes (32 KB by default), so units stay comparable in size and long rows
+// or very wide panels are split into pieces.
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -41,28 +41,23 @@ __global__ void k_pack_panels(const PanelDesc* pd, const T* tval, int vec, T* pv
   }
 }
 
-int64_t env_i64(const char* name, int64_t dflt) {
-  const char* s = getenv(name);
-  return s && *s ? atoll(s) : dflt;
-}
-
 // Upper bound of the 16-byte-aligned cover of `bytes` bytes.
 constexpr int64_t cover(int64_t bytes) { return bytes > 0 ? bytes + 32 : 0; }
 
 }  // namespace
 
-// Plan budgets (SABLE_U* environment overrides are for tuning runs only).
+// Plan budgets (from the executor configuration, inspect.cu exec_config).
 struct UnitBudget {
-  int64_t stage;        // bytes of one unit's data (one executor stage)
+  int64_t stage;        // cap on one unit's bytes (its data's aligned covers)
   int64_t rem_rows;     // rows per remainder-only unit (<= 32)
-  int64_t batch_units;  // units per warp batch (the executor's pipeline length)
+  int64_t batch_units;  // units per warp batch
 };
 
-UnitBudget unit_budget(bool staged) {
+UnitBudget unit_budget(const ExecCfg& c) {
   UnitBudget b;
-  b.stage = env_i64("SABLE_USTAGE", staged ? kUnitStage : kUnitBytes);
-  b.rem_rows = std::min<int64_t>(32, std::max<int64_t>(1, env_i64("SABLE_UREM_ROWS", 32)));
-  b.batch_units = std::max<int64_t>(1, env_i64("SABLE_UBATCH_UNITS", 4));
+  b.stage = c.ustage;
+  b.rem_rows = c.rem_rows;
+  b.batch_units = c.batch;
   return b;
 }
 
@@ -75,22 +70,20 @@ int choose_llpr(int64_t wq) {
 }
 
 template <typename T>
-cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vector<int32_t>& H_rpntr,
-                       const std::vector<int32_t>& H_W, const std::vector<int64_t>& br_vbase,
-                       const std::vector<int64_t>& br_wprefix, const std::vector<int64_t>& br_t0,
-                       const std::vector<int32_t>& H_rp, const std::vector<XTile>& H_xt,
+cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
+                       const std::vector<int32_t>& H_rpntr, const std::vector<int32_t>& H_W,
+                       const std::vector<int64_t>& br_vbase, const std::vector<int64_t>& br_wprefix,
+                       const std::vector<int64_t>& br_t0, const std::vector<int32_t>& H_rp,
+                       const std::vector<XTile>& H_xt, std::vector<int64_t>& br_pbase,
                        cudaStream_t st) {
   const int64_t sv = sizeof(T), vec = 16 / sv, ent = 4 + sv;
-  const UnitBudget B = unit_budget(h->cfg.ustaged != 0);
+  const UnitBudget B = unit_budget(h->cfg);
+  br_pbase.assign((size_t)nbl + 1, 0);
   const int64_t S = B.stage;
   auto rp_bytes = [](int64_t nr) { return cover((nr + 1) * 4); };
   auto rem_cap = [&](int64_t nr) {  // entries of a remainder-only unit of nr rows
     return std::max<int64_t>(1, (S - rp_bytes(nr) - 64) / ent);
   };
-  if (S < 1024 || S % 16 || rem_cap(32) < 32) {
-    set_error("SABLE_USTAGE must be a multiple of 16 and >= 1024");
-    return cudaErrorInvalidValue;
-  }
   std::vector<Unit> U;
   std::vector<int32_t> xq;     // x map, one entry per column vector
   std::vector<int32_t> xside;  // 4 columns per straddling column vector
@@ -160,6 +153,7 @@ cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vect
     const int32_t hgt = H_rpntr[a + 1] - H_rpntr[a];
     const int32_t r0 = (int32_t)(H_rpntr[a] - h->row_begin);
     const int32_t W = H_W[a];
+    br_pbase[la] = pb;
     if (W == 0) {
       if (pend < 0) pend = r0;
       continue;
@@ -262,14 +256,40 @@ cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vect
   }
   const int64_t nloc = (int64_t)H_rp.size() - 1;
   if (pend >= 0) emit_rem_rows(pend, (int32_t)nloc);
+  br_pbase[nbl] = pb;
   if (pb / vec > INT32_MAX || (int64_t)xq.size() > INT32_MAX || (int64_t)U.size() > INT32_MAX) {
     set_error("unit plan exceeds 2^31 vectors, x map entries or units");
     return cudaErrorInvalidValue;
   }
 
-  // warp batches: runs of consecutive units (a warp pipelines its batch)
+  // exchange slices: kSlices runs of consecutive units of about equal bytes,
+  // cut only where a row range starts (never inside a combine group), so a
+  // slice's rows are final when its launch ends (comm.cu overlaps their
+  // all-gather with the next slice); then warp batches of batch_units
+  // consecutive units inside each slice
+  std::vector<int64_t> ucut(1, 0);
+  {
+    int64_t tot = 0;
+    for (const Unit& u : U) tot += (int64_t)u.nr * u.wq * 16 + (int64_t)(u.e1 - u.e0) * ent + 64;
+    int64_t acc = 0;
+    for (size_t i = 0; i < U.size(); ++i) {
+      const int s = (int)ucut.size();  // next boundary index
+      const bool starts = U[i].xg < 0 || U[i].piece == 0;
+      if (s < kSlices && starts && i > 0 && acc * kSlices >= tot * s) ucut.push_back((int64_t)i);
+      acc += (int64_t)U[i].nr * U[i].wq * 16 + (int64_t)(U[i].e1 - U[i].e0) * ent + 64;
+    }
+    while ((int)ucut.size() < kSlices + 1) ucut.push_back((int64_t)U.size());
+  }
   std::vector<int32_t> batch;
-  for (size_t i = 0; i < U.size(); i += (size_t)B.batch_units) batch.push_back((int32_t)i);
+  h->slice_batch.assign(kSlices + 1, 0);
+  h->slice_row.assign(kSlices + 1, 0);
+  for (int s = 0; s < kSlices; ++s) {
+    h->slice_batch[s] = (int64_t)batch.size();
+    h->slice_row[s] = ucut[s] < (int64_t)U.size() ? U[ucut[s]].row0 : nloc;
+    for (int64_t i = ucut[s]; i < ucut[s + 1]; i += B.batch_units) batch.push_back((int32_t)i);
+  }
+  h->slice_batch[kSlices] = (int64_t)batch.size();
+  h->slice_row[kSlices] = nloc;
   batch.push_back((int32_t)U.size());
 
   // upload
@@ -280,7 +300,7 @@ cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vect
   h->n_xside = (int64_t)xside.size() / 4;
   h->n_uxg = (int64_t)xg.size();
   h->pv_elems = pb;
-  h->ustage = (int32_t)S;
+  h->uscratch_slots = slot;
   auto up = [&](void** dst, const void* src, size_t bytes) {
     if (e) return;
     e = cudaMalloc(dst, bytes ? bytes : 16);
@@ -301,7 +321,7 @@ cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vect
     e = cudaMalloc(reinterpret_cast<void**>(&pd_d), sizeof(PanelDesc) * pd.size());
     if (!e) e = cudaMemcpyAsync(pd_d, pd.data(), sizeof(PanelDesc) * pd.size(), cudaMemcpyHostToDevice, st);
     if (!e) {
-      k_pack_panels<T><<<(unsigned)pd.size(), 256, 0, st>>>(pd_d, static_cast<const T*>(h->tval),
+      k_pack_panels<T><<<(unsigned)pd.size(), 256, 0, st>>>(pd_d, tval,
                                                            (int)vec, static_cast<T*>(h->pv));
       e = cudaGetLastError();
     }
@@ -312,15 +332,13 @@ cudaError_t plan_units(sable_handle* h, int32_t nbl, int32_t b0, const std::vect
   return e;
 }
 
-template cudaError_t plan_units<float>(sable_handle*, int32_t, int32_t, const std::vector<int32_t>&,
-                                       const std::vector<int32_t>&, const std::vector<int64_t>&,
-                                       const std::vector<int64_t>&, const std::vector<int64_t>&,
-                                       const std::vector<int32_t>&, const std::vector<XTile>&,
-                                       cudaStream_t);
-template cudaError_t plan_units<double>(sable_handle*, int32_t, int32_t, const std::vector<int32_t>&,
-                                        const std::vector<int32_t>&, const std::vector<int64_t>&,
-                                        const std::vector<int64_t>&, const std::vector<int64_t>&,
-                                        const std::vector<int32_t>&, const std::vector<XTile>&,
-                                        cudaStream_t);
+#define SABLE_PLAN_INST(T)                                                                  \
+  template cudaError_t plan_units<T>(                                                      \
+      sable_handle*, const T*, int32_t, int32_t, const std::vector<int32_t>&,              \
+      const std::vector<int32_t>&, const std::vector<int64_t>&, const std::vector<int64_t>&, \
+      const std::vector<int64_t>&, const std::vector<int32_t>&, const std::vector<XTile>&,  \
+      std::vector<int64_t>&, cudaStream_t);
+SABLE_PLAN_INST(float)
+SABLE_PLAN_INST(double)
 
 }  // namespace sable

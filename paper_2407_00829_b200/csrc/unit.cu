@@ -1,5 +1,6 @@
 // unit.cu -- the SpMV executor: y = A x over the VBR-C split in ONE launch
-// (north_star (2)).
+// (north_star (2)), and its multi-vector form Y = A X
+// for KV = 2, 4, 8 right-hand sides on the same plan.
 //
 // y_i = sum_j A_ij x_j, evaluated per row as
 //   y_r = sum over the dense tiles of r's block row  T(r, c) x_c      (dense)
@@ -31,95 +32,29 @@
 //               summed by the whole warp with a fixed tree).
 //   y           lane r writes y_r = dense_r + rem_r once: no atomics, no
 //               read-modify-write, no second launch.  Rows split over several
-//               units (very long remainder rows) meet in scratch and the last
-//               piece to arrive sums the pieces in piece order.
-// Every row's summation order is fixed by the matrix alone (the plan depends
-// on the block row, never on the shard count or on timing), so y is bitwise
-// reproducible and identical for every P.
-#include "sable_internal.cuh"
+//               units (very long remainder rows, very wide panels) meet in
+//               scratch and the last piece to arrive sums the pieces in piece
+//               order.
+// While a unit computes, lane 0 pulls the next unit's data into L2 with bulk
+// prefetches (cp.async.bulk.prefetch.L2).  Every row's summation order is
+// fixed by the matrix alone (the plan depends on the block row, never on the
+// shard count or on timing), so y is bitwise reproducible and identical for
+// every P.
+#include <algorithm>
+
+#include "device.cuh"
 
 namespace sable {
 
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
+using namespace dev;
+
 constexpr int kUnitThreads = kUnitWarps * 32;
 #ifndef SABLE_UNIT_MINW
 #define SABLE_UNIT_MINW 32  // A/B builds: resident warps per SM asked of ptxas (64 regs)
 #endif
 constexpr int kUnitMinBlocks = SABLE_UNIT_MINW / kUnitWarps;
-
-template <typename T>
-struct Vec;
-template <>
-struct Vec<float> {
-  using V = float4;
-  static constexpr int N = 4;
-  static __device__ __forceinline__ float get(const float4& v, int i) {
-    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-  }
-  static __device__ __forceinline__ float4 zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
-};
-template <>
-struct Vec<double> {
-  using V = double2;
-  static constexpr int N = 2;
-  static __device__ __forceinline__ double get(const double2& v, int i) {
-    return i == 0 ? v.x : v.y;
-  }
-  static __device__ __forceinline__ double2 zero() { return make_double2(0.0, 0.0); }
-};
-
-__device__ __forceinline__ int atom_add_acq_rel(int32_t* p, int v) {
-  int old;
-  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-
-__device__ __forceinline__ Unit load_unit(const Unit* p) {
-  const int4* q = reinterpret_cast<const int4*>(p);
-  const int4 a = __ldg(q), b = __ldg(q + 1);
-  Unit u;
-  u.voff16 = a.x;
-  u.row0 = a.y;
-  u.wq = a.z;
-  u.xq0 = a.w;
-  u.e0 = b.x;
-  u.e1 = b.y;
-  u.xg = b.z;
-  u.nr = (uint8_t)(b.w & 0xff);
-  u.llpr = (uint8_t)((b.w >> 8) & 0xff);
-  u.piece = (uint16_t)((uint32_t)b.w >> 16);
-  return u;
-}
-
-// Predicated streaming 16-byte load (ld.global.cs: evict-first).  Volatile
-// so that a unit's loads are issued in program order, all before the first
-// multiply-add that waits on them; with the predicate off, v keeps its old
-// value (the callers never read a row past nr).
-__device__ __forceinline__ void ld_cs_if(float4& v, const float4* p, bool pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-      "@q ld.global.cs.v4.f32 {%0, %1, %2, %3}, [%4];\n}"
-      : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
-      : "l"(p), "r"((int)pred));
-}
-__device__ __forceinline__ void ld_cs_if(double2& v, const double2* p, bool pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
-      "@q ld.global.cs.v2.f64 {%0, %1}, [%2];\n}"
-      : "+d"(v.x), "+d"(v.y)
-      : "l"(p), "r"((int)pred));
-}
-
-// Bulk L2 prefetch (UBLKPF) of the 16-byte-aligned cover of [p, p + bytes).
-__device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
-  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + (uintptr_t)bytes + 15) & ~uintptr_t(15);
-  if (bytes > 0)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a))
-                 : "memory");
-}
 
 // Lane 0: pull a unit's data (dense rows, x map, remainder row pointers,
 // columns and values) into L2 while the previous unit computes, so the
@@ -137,21 +72,23 @@ __device__ __forceinline__ void prefetch_unit(const UPlan<T>& P, const Unit& U) 
   }
 }
 
-// x of the N columns of panel column vector q (x map entry m).
-template <typename T>
+// x (row-major ncols x KV) of the N columns of one panel column vector,
+// x map entry m (>= 0: columns m, m + 1, ... clamped to ncols - 1; < 0: the
+// side entry ~m lists the N columns).
+template <typename T, int KV>
 __device__ __forceinline__ void load_xv(const UPlan<T>& P, int m, const T* __restrict__ x,
-                                        T (&xv)[Vec<T>::N]) {
+                                        T (&xv)[Vec<T>::N][KV]) {
   constexpr int N = Vec<T>::N;
   if (m >= 0) {
 #pragma unroll
-    for (int i = 0; i < N; ++i) xv[i] = __ldg(x + min(m + i, P.nm1));
+    for (int i = 0; i < N; ++i) ldg_kv<T, KV>(x + (int64_t)min(m + i, P.nm1) * KV, xv[i]);
   } else {
     const int4 c = __ldg(P.xside + ~m);
-    xv[0] = __ldg(x + c.x);
-    xv[1] = __ldg(x + c.y);
+    ldg_kv<T, KV>(x + (int64_t)c.x * KV, xv[0]);
+    ldg_kv<T, KV>(x + (int64_t)c.y * KV, xv[1]);
     if constexpr (N == 4) {
-      xv[2] = __ldg(x + c.z);
-      xv[3] = __ldg(x + c.w);
+      ldg_kv<T, KV>(x + (int64_t)c.z * KV, xv[2]);
+      ldg_kv<T, KV>(x + (int64_t)c.w * KV, xv[3]);
     }
   }
 }
@@ -180,49 +117,68 @@ __device__ __forceinline__ void fold_lanes(T (&acc)[K], int lane) {
   }
 }
 
-// Dense part of a unit with LPR lanes per row: returns row `lane`'s sum
-// (valid for lane < nr).  Lane (sub, ql) takes rows sub, sub + SUB, ... (at
-// most K = min(LPR, 8)) and column vectors ql, ql + LPR, ...; row sub + SUB*k
-// ends in lane sub * LPR + k * (LPR / K).
-template <typename T, int LPR>
-__device__ __forceinline__ T dense_rows(const UPlan<T>& P, const Unit& U,
-                                        const T* __restrict__ x, int lane) {
+// Dense part of a unit with LPR lanes per row: out[j] = row `lane`'s sum
+// for vector j (valid for lane < nr).  Lane (sub, ql) takes column vectors
+// ql, ql + LPR, ... of rows sub, sub + SUB, ...: K = min(LPR, 8) / KV of them
+// per row pass (KV = 1: one pass), and row sub + SUB * (p * K + k) ends in
+// lane sub * LPR + k * (LPR / K) after pass p's fold.
+template <typename T, int LPR, int KV>
+__device__ __forceinline__ void dense_rows(const UPlan<T>& P, const Unit& U,
+                                           const T* __restrict__ x, int lane, T (&out)[KV]) {
   using V = typename Vec<T>::V;
   constexpr int N = Vec<T>::N;
   constexpr int SUB = 32 / LPR;
-  constexpr int K = LPR < 8 ? LPR : 8;
+  constexpr int K8 = LPR < 8 ? LPR : 8;
+  constexpr int K = K8 / KV > 0 ? K8 / KV : 1;
+  constexpr int RP = K8 / K;  // row passes
   const int sub = lane / LPR, ql = lane % LPR;
   const int wq = U.wq, nr = U.nr;
   const V* vp = reinterpret_cast<const V*>(P.pv) + U.voff16 + sub * wq;
   const int* xm = P.xq + U.xq0;
-  T acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = T(0);
   const int64_t rstep = (int64_t)SUB * wq;
-  V v[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = Vec<T>::zero();
 #pragma unroll 1
-  for (int q = ql; q < wq; q += LPR) {
-    // the rows' values first (independent of x; rows past nr are not loaded
-    // and their accumulators are never read), then x of the lane's columns,
-    // then the multiply-adds in column order
-    const V* p = vp + q;
+  for (int rp = 0; rp < RP; ++rp) {
+    if (SUB * rp * K >= nr) break;  // no lane has a row in this pass
+    const int rb = sub + SUB * rp * K;
+    T acc[KV][K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      ld_cs_if(v[k], p, sub + SUB * k < nr);
-      p += rstep;
+    for (int j = 0; j < KV; ++j)
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[j][k] = T(0);
+    V v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = Vec<T>::zero();
+#pragma unroll 1
+    for (int q = ql; q < wq; q += LPR) {
+      // the rows' values first (independent of x; rows past nr are not
+      // loaded and their accumulators are never read), then x of the lane's
+      // columns, then the multiply-adds in column order
+      const V* p = vp + q + rp * K * rstep;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        ld_cs_if(v[k], p, rb + SUB * k < nr);
+        p += rstep;
+      }
+      T xv[N][KV];
+      load_xv<T, KV>(P, __ldg(xm + q), x, xv);
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+#pragma unroll
+          for (int j = 0; j < KV; ++j)
+            acc[j][k] = fma(Vec<T>::get(v[k], i), xv[i][j], acc[j][k]);
     }
-    T xv[N];
-    load_xv<T>(P, __ldg(xm + q), x, xv);
 #pragma unroll
-    for (int k = 0; k < K; ++k)
+    for (int j = 0; j < KV; ++j) fold_lanes<LPR / 2, K>(acc[j], lane);
+    const int kk = lane / SUB - rp * K;
+    const int src = (lane % SUB) * LPR + kk * (LPR / K);
 #pragma unroll
-      for (int i = 0; i < N; ++i) acc[k] = fma(Vec<T>::get(v[k], i), xv[i], acc[k]);
+    for (int j = 0; j < KV; ++j) {
+      const T t = __shfl_sync(kFull, acc[j][0], src & 31);
+      if (kk >= 0 && kk < K) out[j] = t;
+    }
   }
-  fold_lanes<LPR / 2, K>(acc, lane);
-  const int src = (lane % SUB) * LPR + (lane / SUB) * (LPR / K);
-  return __shfl_sync(kFull, acc[0], src & 31);
 }
 
 // Remainder part in waves of kRemWave entries (kRemKB coalesced loads per
@@ -254,9 +210,10 @@ __device__ __forceinline__ void rem_load(const UPlan<T>& P, int c0, int e1, int 
   }
 }
 
-template <typename T>
-__device__ __forceinline__ T rem_rows(const UPlan<T>& P, const Unit& U, const T* __restrict__ x,
-                                      T* buf, int lane) {
+template <typename T, int KV>
+__device__ __forceinline__ void rem_rows(const UPlan<T>& P, const Unit& U,
+                                         const T* __restrict__ x, T* buf, int lane,
+                                         T (&s)[KV]) {
   int lo = 0, hi = 0;
   if (lane < U.nr) {
     lo = max(__ldg(P.rptr + U.row0 + lane), U.e0);
@@ -264,44 +221,91 @@ __device__ __forceinline__ T rem_rows(const UPlan<T>& P, const Unit& U, const T*
   }
   RemWave<T> w;
   rem_load(P, U.e0, U.e1, lane, w);
-  T s = T(0);
 #pragma unroll 1
   for (int c0 = U.e0; c0 < U.e1; c0 += kRemWave) {
     const int n = min(kRemWave, U.e1 - c0);
-    T pr[kRemKB];
+    T pr[kRemKB][KV];
 #pragma unroll
-    for (int k = 0; k < kRemKB; ++k) pr[k] = (k * 32 + lane < n) ? w.v[k] * __ldg(x + w.c[k]) : T(0);
+    for (int k = 0; k < kRemKB; ++k) {
+      T xg[KV];
+#pragma unroll
+      for (int j = 0; j < KV; ++j) xg[j] = T(0);
+      if (k * 32 + lane < n) ldg_kv<T, KV>(x + (int64_t)w.c[k] * KV, xg);
+#pragma unroll
+      for (int j = 0; j < KV; ++j) pr[k][j] = w.v[k] * xg[j];
+    }
     if (c0 + kRemWave < U.e1) rem_load(P, c0 + kRemWave, U.e1, lane, w);
 #pragma unroll
     for (int k = 0; k < kRemKB; ++k)
-      if (k * 32 + lane < n) buf[k * 32 + lane] = pr[k];
+      if (k * 32 + lane < n)
+#pragma unroll
+        for (int j = 0; j < KV; ++j) buf[(k * 32 + lane) * KV + j] = pr[k][j];
     __syncwarp();
     const int a = max(lo, c0) - c0, b = min(hi, c0 + n) - c0;
     const bool longr = b - a > 32;
     if (!longr)
-      for (int e = a; e < b; ++e) s += buf[e];
+      for (int e = a; e < b; ++e)
+#pragma unroll
+        for (int j = 0; j < KV; ++j) s[j] += buf[e * KV + j];
     unsigned lm = __ballot_sync(kFull, longr);
     while (lm) {
       const int q = __ffs(lm) - 1;
       lm &= lm - 1;
       const int a2 = __shfl_sync(kFull, a, q), b2 = __shfl_sync(kFull, b, q);
-      T t = T(0);
-      for (int e = a2 + lane; e < b2; e += 32) t += buf[e];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
-      if (lane == q) s += t;
+      for (int j = 0; j < KV; ++j) {
+        T t = T(0);
+        for (int e = a2 + lane; e < b2; e += 32) t += buf[e * KV + j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
+        if (lane == q) s[j] += t;
+      }
     }
     __syncwarp();
   }
-  return s;
 }
 
-template <typename T>
+// y of a unit's rows (row-major nloc x KV), or its partials into the
+// combine group (the last piece to arrive sums the pieces in order).
+template <typename T, int KV>
+__device__ __forceinline__ void finish_unit(const UPlan<T>& P, const Unit& U, const T (&s)[KV],
+                                            T* __restrict__ y, int lane) {
+  if (U.xg < 0) {
+    if (lane < U.nr)
+#pragma unroll
+      for (int j = 0; j < KV; ++j) y[(int64_t)(U.row0 + lane) * KV + j] = s[j];
+    return;
+  }
+  const int4 gv = __ldg(reinterpret_cast<const int4*>(P.xg + U.xg));
+  const int64_t slot = (int64_t)(((uint64_t)(uint32_t)gv.y << 32) | (uint32_t)gv.x);
+  const int counter = gv.z, np = gv.w;
+  T* sp = P.scratch + slot * KV;
+  if (lane < U.nr)
+#pragma unroll
+    for (int j = 0; j < KV; ++j) __stcg(sp + (U.piece * 32 + lane) * KV + j, s[j]);
+  __syncwarp();  // the warp's partials before lane 0's release
+  int last = 0;
+  if (lane == 0) last = (atom_add_acq_rel(P.counters + counter, 1) + 1 == np);
+  last = __shfl_sync(kFull, last, 0);
+  if (last) {
+    if (lane < U.nr) {
+#pragma unroll
+      for (int j = 0; j < KV; ++j) {
+        T t = __ldcg(sp + lane * KV + j);
+        for (int q = 1; q < np; ++q) t += __ldcg(sp + (q * 32 + lane) * KV + j);
+        y[(int64_t)(U.row0 + lane) * KV + j] = t;
+      }
+    }
+    if (lane == 0) P.counters[counter] = 0;  // ready for the next launch
+  }
+}
+
+template <typename T, int KV>
 __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
     unit_kernel(const __grid_constant__ UPlan<T> P, const T* __restrict__ x, T* __restrict__ y) {
-  __shared__ __align__(16) T buf_s[kUnitWarps][kRemWave];
+  __shared__ __align__(16) T buf_s[kUnitWarps][kRemWave * KV];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t b = (int64_t)blockIdx.x * kUnitWarps + warp;
+  const int64_t b = P.b0 + (int64_t)blockIdx.x * kUnitWarps + warp;
   if (b >= P.n_batches) return;
   const int u0 = __ldg(P.batch + b), u1 = __ldg(P.batch + b + 1);
   if (lane == 0 && P.pf) l2_prefetch(P.units + u0, (int64_t)(u1 - u0) * sizeof(Unit));
@@ -309,325 +313,27 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
   for (int u = u0; u < u1; ++u) {
     const Unit U = Un;
     if (u + 1 < u1) Un = load_unit(P.units + u + 1);
-    T s = T(0);
+    T s[KV];
+#pragma unroll
+    for (int j = 0; j < KV; ++j) s[j] = T(0);
     if (U.wq > 0) {
       switch (U.llpr) {
-        case 0: s = dense_rows<T, 1>(P, U, x, lane); break;
-        case 1: s = dense_rows<T, 2>(P, U, x, lane); break;
-        case 2: s = dense_rows<T, 4>(P, U, x, lane); break;
-        case 3: s = dense_rows<T, 8>(P, U, x, lane); break;
-        case 4: s = dense_rows<T, 16>(P, U, x, lane); break;
-        default: s = dense_rows<T, 32>(P, U, x, lane); break;
+        case 0: dense_rows<T, 1, KV>(P, U, x, lane, s); break;
+        case 1: dense_rows<T, 2, KV>(P, U, x, lane, s); break;
+        case 2: dense_rows<T, 4, KV>(P, U, x, lane, s); break;
+        case 3: dense_rows<T, 8, KV>(P, U, x, lane, s); break;
+        case 4: dense_rows<T, 16, KV>(P, U, x, lane, s); break;
+        default: dense_rows<T, 32, KV>(P, U, x, lane, s); break;
       }
     }
     if (lane == 0 && P.pf && u + 1 < u1) prefetch_unit(P, Un);
-    if (U.e1 > U.e0) s += rem_rows<T>(P, U, x, buf_s[warp], lane);
-    if (U.xg < 0) {
-      if (lane < U.nr) y[U.row0 + lane] = s;
-    } else {
-      const int4 gv = __ldg(reinterpret_cast<const int4*>(P.xg + U.xg));
-      const int64_t slot = (int64_t)(((uint64_t)(uint32_t)gv.y << 32) | (uint32_t)gv.x);
-      const int counter = gv.z, np = gv.w;
-      T* sp = P.scratch + slot;
-      if (lane < U.nr) __stcg(sp + U.piece * 32 + lane, s);
-      __syncwarp();  // the warp's partials before lane 0's release
-      int last = 0;
-      if (lane == 0) last = (atom_add_acq_rel(P.counters + counter, 1) + 1 == np);
-      last = __shfl_sync(kFull, last, 0);
-      if (last) {
-        if (lane < U.nr) {
-          T t = __ldcg(sp + lane);
-          for (int q = 1; q < np; ++q) t += __ldcg(sp + q * 32 + lane);
-          y[U.row0 + lane] = t;
-        }
-        if (lane == 0) P.counters[counter] = 0;  // ready for the next launch
-      }
-    }
+    if (U.e1 > U.e0) rem_rows<T, KV>(P, U, x, buf_s[warp], lane, s);
+    finish_unit<T, KV>(P, U, s, y, lane);
   }
-}
-
-// ------------------------------------------------------------------------
-// The staged executor (default): every warp pipelines its batch of units
-// through two shared-memory stages.  Lane 0 pulls unit u + 1's data -- dense
-// rows, x map, remainder row pointers, columns and values, each the
-// 16-byte-aligned cover of its range -- with cp.async.bulk copies completing
-// on the stage's mbarrier while the warp computes unit u from the other
-// stage, so the HBM latency of a unit is hidden behind the previous one and
-// no register holds a value in flight.  Per unit, only x (L2-resident) is
-// read from global memory.
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
-      : "memory");
-}
-
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
-// Where a unit's regions sit in its stage (bytes), and the element offset of
-// each range's first element inside its 16-byte-aligned cover.
-struct StageMap {
-  uint32_t o_xm, o_rp, o_ix, o_rv, total;
-  uint32_t d_xm, d_rp, d_ix, d_rv;
-};
-
-template <typename T>
-__device__ __forceinline__ StageMap stage_map(const UPlan<T>& P, const Unit& U) {
-  StageMap m{};
-  uint32_t off = U.wq > 0 ? (uint32_t)U.nr * (uint32_t)U.wq * 16u : 0u;
-  auto region = [&](const void* p, uint32_t bytes, uint32_t esz, uint32_t& o, uint32_t& d) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    const uint32_t c = bytes ? (uint32_t)(((a + bytes + 15) & ~uintptr_t(15)) - (a & ~uintptr_t(15))) : 0u;
-    o = off;
-    d = (uint32_t)(a & 15) / esz;
-    off += c;
-  };
-  if (U.wq > 0) region(P.xq + U.xq0, (uint32_t)U.wq * 4u, 4u, m.o_xm, m.d_xm);
-  const uint32_t ne = (uint32_t)(U.e1 - U.e0);
-  if (ne > 0) {
-    region(P.rptr + U.row0, ((uint32_t)U.nr + 1u) * 4u, 4u, m.o_rp, m.d_rp);
-    region(P.ridx + U.e0, ne * 4u, 4u, m.o_ix, m.d_ix);
-    region(P.rval + U.e0, ne * (uint32_t)sizeof(T), (uint32_t)sizeof(T), m.o_rv, m.d_rv);
-  }
-  m.total = off;
-  return m;
-}
-
-// Lane 0: start the bulk copies of a unit's data into a stage.
-template <typename T>
-__device__ __forceinline__ void issue_unit(const UPlan<T>& P, const Unit& U, unsigned char* stage,
-                                           uint32_t bar, uint64_t pol) {
-  const StageMap m = stage_map(P, U);
-  mbar_expect_tx(bar, m.total);
-  const uint32_t s0 = smem_u32(stage);
-  auto cp = [&](const void* p, uint32_t bytes, uint32_t o) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
-    const uint32_t c = (uint32_t)(((reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15)) - a);
-    bulk_g2s(s0 + o, reinterpret_cast<const void*>(a), c, bar, pol);
-  };
-  if (U.wq > 0) {
-    cp(reinterpret_cast<const uint4*>(P.pv) + U.voff16, (uint32_t)U.nr * (uint32_t)U.wq * 16u, 0u);
-    cp(P.xq + U.xq0, (uint32_t)U.wq * 4u, m.o_xm);
-  }
-  const uint32_t ne = (uint32_t)(U.e1 - U.e0);
-  if (ne > 0) {
-    cp(P.rptr + U.row0, ((uint32_t)U.nr + 1u) * 4u, m.o_rp);
-    cp(P.ridx + U.e0, ne * 4u, m.o_ix);
-    cp(P.rval + U.e0, ne * (uint32_t)sizeof(T), m.o_rv);
-  }
-}
-
-// Dense part from a stage (same lane mapping and tree as dense_rows).
-template <typename T, int LPR>
-__device__ __forceinline__ T dense_staged(const UPlan<T>& P, const Unit& U, const StageMap& m,
-                                          const unsigned char* stage, const T* __restrict__ x,
-                                          int lane) {
-  using V = typename Vec<T>::V;
-  constexpr int N = Vec<T>::N;
-  constexpr int SUB = 32 / LPR;
-  constexpr int K = LPR < 8 ? LPR : 8;
-  const int sub = lane / LPR, ql = lane % LPR;
-  const int wq = U.wq, nr = U.nr;
-  const V* vs = reinterpret_cast<const V*>(stage) + sub * wq;
-  const int* xm = reinterpret_cast<const int*>(stage + m.o_xm) + m.d_xm;
-  T acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = T(0);
-#pragma unroll 1
-  for (int q = ql; q < wq; q += LPR) {
-    T xv[N];
-    load_xv<T>(P, xm[q], x, xv);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (sub + SUB * k < nr) {
-        const V v = vs[q + k * SUB * wq];
-#pragma unroll
-        for (int i = 0; i < N; ++i) acc[k] = fma(Vec<T>::get(v, i), xv[i], acc[k]);
-      }
-    }
-  }
-  fold_lanes<LPR / 2, K>(acc, lane);
-  const int src = (lane % SUB) * LPR + (lane / SUB) * (LPR / K);
-  return __shfl_sync(kFull, acc[0], src & 31);
-}
-
-// Remainder part from a stage: the products of a wave (8 per lane) go to
-// `buf`, lane r sums row r's in entry order (long rows: the whole warp, a
-// fixed tree).
-constexpr int kSRemKB = 8;
-constexpr int kSRemWave = 32 * kSRemKB;
-
-template <typename T>
-__device__ __forceinline__ T rem_staged(const UPlan<T>& P, const Unit& U, const StageMap& m,
-                                        const unsigned char* stage, const T* __restrict__ x,
-                                        T* buf, int lane) {
-  const int ne = U.e1 - U.e0;
-  const int* rp = reinterpret_cast<const int*>(stage + m.o_rp) + m.d_rp;
-  const int* ix = reinterpret_cast<const int*>(stage + m.o_ix) + m.d_ix;
-  const T* rv = reinterpret_cast<const T*>(stage + m.o_rv) + m.d_rv;
-  int lo = 0, hi = 0;
-  if (lane < U.nr) {
-    lo = max(rp[lane] - U.e0, 0);
-    hi = min(rp[lane + 1] - U.e0, ne);
-  }
-  T s = T(0);
-#pragma unroll 1
-  for (int c0 = 0; c0 < ne; c0 += kSRemWave) {
-    const int n = min(kSRemWave, ne - c0);
-    T xg[kSRemKB];
-#pragma unroll
-    for (int k = 0; k < kSRemKB; ++k) {
-      const int e = k * 32 + lane;
-      xg[k] = e < n ? __ldg(x + ix[c0 + e]) : T(0);
-    }
-#pragma unroll
-    for (int k = 0; k < kSRemKB; ++k) {
-      const int e = k * 32 + lane;
-      if (e < n) buf[e] = rv[c0 + e] * xg[k];
-    }
-    __syncwarp();
-    const int a = max(lo, c0) - c0, b = min(hi, c0 + n) - c0;
-    const bool longr = b - a > 32;
-    if (!longr)
-      for (int e = a; e < b; ++e) s += buf[e];
-    unsigned lm = __ballot_sync(kFull, longr);
-    while (lm) {
-      const int q = __ffs(lm) - 1;
-      lm &= lm - 1;
-      const int a2 = __shfl_sync(kFull, a, q), b2 = __shfl_sync(kFull, b, q);
-      T t = T(0);
-      for (int e = a2 + lane; e < b2; e += 32) t += buf[e];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o);
-      if (lane == q) s += t;
-    }
-    __syncwarp();
-  }
-  return s;
-}
-
-// y of a unit's rows (or its partials into the combine group).
-template <typename T>
-__device__ __forceinline__ void finish_unit(const UPlan<T>& P, const Unit& U, T s,
-                                            T* __restrict__ y, int lane) {
-  if (U.xg < 0) {
-    if (lane < U.nr) y[U.row0 + lane] = s;
-    return;
-  }
-  const int4 gv = __ldg(reinterpret_cast<const int4*>(P.xg + U.xg));
-  const int64_t slot = (int64_t)(((uint64_t)(uint32_t)gv.y << 32) | (uint32_t)gv.x);
-  const int counter = gv.z, np = gv.w;
-  T* sp = P.scratch + slot;
-  if (lane < U.nr) __stcg(sp + U.piece * 32 + lane, s);
-  __syncwarp();  // the warp's partials before lane 0's release
-  int last = 0;
-  if (lane == 0) last = (atom_add_acq_rel(P.counters + counter, 1) + 1 == np);
-  last = __shfl_sync(kFull, last, 0);
-  if (last) {
-    if (lane < U.nr) {
-      T t = __ldcg(sp + lane);
-      for (int q = 1; q < np; ++q) t += __ldcg(sp + q * 32 + lane);
-      y[U.row0 + lane] = t;
-    }
-    if (lane == 0) P.counters[counter] = 0;  // ready for the next launch
-  }
-}
-
-// Shared memory of one warp: 2 mbarriers (16 B), two stages, the products.
-template <typename T>
-__host__ __device__ constexpr uint32_t staged_warp_bytes(uint32_t stage) {
-  return 16u + 2u * stage + (uint32_t)(kSRemWave * sizeof(T));
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
-    unit_staged_kernel(const __grid_constant__ UPlan<T> P, const T* __restrict__ x,
-                       T* __restrict__ y) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t b = (int64_t)blockIdx.x * kUnitWarps + warp;
-  if (b >= P.n_batches) return;
-  unsigned char* ws = smem + (size_t)warp * staged_warp_bytes<T>(P.stage);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ws);
-  unsigned char* stg[2] = {ws + 16, ws + 16 + P.stage};
-  T* buf = reinterpret_cast<T*>(ws + 16 + 2 * P.stage);
-  const int u0 = __ldg(P.batch + b), u1 = __ldg(P.batch + b + 1);
-  uint64_t pol = 0;
-  Unit U = load_unit(P.units + u0);
-  Unit Un = U;
-  if (u0 + 1 < u1) Un = load_unit(P.units + u0 + 1);
-  if (lane == 0) {
-    mbar_init(smem_u32(bar), 1);
-    mbar_init(smem_u32(bar + 1), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    pol = policy_evict_first();
-    issue_unit(P, U, stg[0], smem_u32(bar), pol);
-  }
-  __syncwarp();
-  for (int u = u0; u < u1; ++u) {
-    const int s = (u - u0) & 1;
-    const uint32_t par = (uint32_t)((u - u0) >> 1) & 1u;
-    // unit u + 1's data into the other stage (freed at the end of u - 1)
-    if (lane == 0 && u + 1 < u1) issue_unit(P, Un, stg[s ^ 1], smem_u32(bar + (s ^ 1)), pol);
-    Unit Unn = Un;
-    if (u + 2 < u1) Unn = load_unit(P.units + u + 2);
-    const StageMap m = stage_map(P, U);
-    mbar_wait(smem_u32(bar + s), par);
-    const unsigned char* st = stg[s];
-    T acc = T(0);
-    if (U.wq > 0) {
-      switch (U.llpr) {
-        case 0: acc = dense_staged<T, 1>(P, U, m, st, x, lane); break;
-        case 1: acc = dense_staged<T, 2>(P, U, m, st, x, lane); break;
-        case 2: acc = dense_staged<T, 4>(P, U, m, st, x, lane); break;
-        case 3: acc = dense_staged<T, 8>(P, U, m, st, x, lane); break;
-        case 4: acc = dense_staged<T, 16>(P, U, m, st, x, lane); break;
-        default: acc = dense_staged<T, 32>(P, U, m, st, x, lane); break;
-      }
-    }
-    if (U.e1 > U.e0) acc += rem_staged<T>(P, U, m, st, x, buf, lane);
-    finish_unit(P, U, acc, y, lane);
-    __syncwarp();  // stage s is free for unit u + 2
-    U = Un;
-    Un = Unn;
-  }
-}
-
-}  // namespace
-
-template <typename T>
-cudaError_t launch_units(const sable_handle* h, const void* x, void* y, cudaStream_t st) {
-  if (h->n_ubatch == 0) return cudaSuccess;
+UPlan<T> make_plan(const sable_handle* h, void* scratch) {
   UPlan<T> P;
   P.units = h->units;
   P.batch = h->ubatch;
@@ -638,30 +344,62 @@ cudaError_t launch_units(const sable_handle* h, const void* x, void* y, cudaStre
   P.ridx = h->rem_idx;
   P.rval = static_cast<const T*>(h->rem_val);
   P.xg = h->uxg;
-  P.scratch = static_cast<T*>(h->uscratch);
+  P.scratch = static_cast<T*>(scratch);
   P.counters = h->ucounters;
+  P.b0 = 0;
   P.n_batches = h->n_ubatch;
   P.nm1 = (int32_t)(h->ncols - 1);
-  P.pf = h->cfg.xpf;
-  P.stage = (uint32_t)h->ustage;
-  const int64_t blocks = (h->n_ubatch + kUnitWarps - 1) / kUnitWarps;
-  if (h->cfg.ustaged) {
-    const size_t smem = (size_t)kUnitWarps * staged_warp_bytes<T>(P.stage);
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e) return e;
-    e = set_smem_attr(reinterpret_cast<const void*>(unit_staged_kernel<T>), dev, smem);
-    if (e) return e;
-    unit_staged_kernel<T><<<(unsigned)blocks, kUnitThreads, smem, st>>>(
-        P, static_cast<const T*>(x), static_cast<T*>(y));
-    return cudaGetLastError();
-  }
-  unit_kernel<T><<<(unsigned)blocks, kUnitThreads, 0, st>>>(P, static_cast<const T*>(x),
-                                                            static_cast<T*>(y));
+  P.pf = h->cfg.pf;
+  return P;
+}
+
+// One launch over warp batches [b0, b1).
+template <typename T, int KV>
+cudaError_t launch_kv(const sable_handle* h, const void* x, void* y, void* scratch,
+                      cudaStream_t st, int64_t b0 = 0, int64_t b1 = -1) {
+  if (b1 < 0) b1 = h->n_ubatch;
+  if (b1 <= b0) return cudaSuccess;
+  UPlan<T> P = make_plan<T>(h, scratch);
+  P.b0 = b0;
+  P.n_batches = b1;
+  const int64_t blocks = (b1 - b0 + kUnitWarps - 1) / kUnitWarps;
+  unit_kernel<T, KV><<<(unsigned)blocks, kUnitThreads, 0, st>>>(P, static_cast<const T*>(x),
+                                                                 static_cast<T*>(y));
   return cudaGetLastError();
 }
 
-template cudaError_t launch_units<float>(const sable_handle*, const void*, void*, cudaStream_t);
-template cudaError_t launch_units<double>(const sable_handle*, const void*, void*, cudaStream_t);
+}  // namespace
+
+int32_t exec_grid(const sable_handle* h) {
+  return h ? (int32_t)((h->n_ubatch + kUnitWarps - 1) / kUnitWarps) : 0;
+}
+
+// y = A x (one launch).
+cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st) {
+  return h->dtype == SABLE_F64 ? launch_kv<double, 1>(h, x, y, h->uscratch, st)
+                               : launch_kv<float, 1>(h, x, y, h->uscratch, st);
+}
+
+// y rows of exchange slice s only (its warp batches; comm.cu).
+cudaError_t run_spmv_slice(const sable_handle* h, const void* x, void* y, int s,
+                           cudaStream_t st) {
+  const int64_t b0 = h->slice_batch[s], b1 = h->slice_batch[s + 1];
+  return h->dtype == SABLE_F64 ? launch_kv<double, 1>(h, x, y, h->uscratch, st, b0, b1)
+                               : launch_kv<float, 1>(h, x, y, h->uscratch, st, b0, b1);
+}
+
+// Y = A X for k in {1, 2, 4, 8} right-hand sides (X row-major ncols x k, Y
+// row-major local rows x k); scratch holds k partials per combine slot.
+cudaError_t run_spmm(const sable_handle* h, const void* X, void* Y, int32_t k, void* scratch,
+                     cudaStream_t st) {
+  const bool f64 = h->dtype == SABLE_F64;
+  switch (k) {
+    case 1: return f64 ? launch_kv<double, 1>(h, X, Y, scratch, st) : launch_kv<float, 1>(h, X, Y, scratch, st);
+    case 2: return f64 ? launch_kv<double, 2>(h, X, Y, scratch, st) : launch_kv<float, 2>(h, X, Y, scratch, st);
+    case 4: return f64 ? launch_kv<double, 4>(h, X, Y, scratch, st) : launch_kv<float, 4>(h, X, Y, scratch, st);
+    case 8: return f64 ? launch_kv<double, 8>(h, X, Y, scratch, st) : launch_kv<float, 8>(h, X, Y, scratch, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 }  // namespace sable

@@ -36,7 +36,7 @@ EXPORTS = ("sable_vbr_create", "sable_spmv", "sable_spmv_host", "sable_destroy",
            "sable_nccl_unique_id", "sable_comm_init", "sable_spmv_allgather",
            "sable_spmv_iterate", "sable_status_string", "sable_last_error",
            "sable_abi_version", "sable_partition_grid", "sable_serialize",
-           "sable_deserialize", "sable_spmm")
+           "sable_deserialize", "sable_spmm", "sable_comm_check", "sable_exchange_rows")
 
 
 class sable_vbr_desc(C.Structure):
@@ -62,14 +62,9 @@ class sable_info(C.Structure):
                 ("nnz", C.c_int64), ("n_cells", C.c_int64), ("cell_base", C.c_int64),
                 ("n_dense", C.c_int64), ("tile_elems", C.c_int64), ("rem_nnz", C.c_int64),
                 ("n_dense_global", C.c_int64), ("bytes_alg", C.c_int64),
-                ("n_groups", C.c_int64), ("n_items", C.c_int64),
                 ("dtype", C.c_int32), ("delta", C.c_int32), ("suitable", C.c_int32),
                 ("world", C.c_int32), ("rank", C.c_int32), ("inspect_ms", C.c_double),
-                ("n_tasks", C.c_int64), ("exec_grid", C.c_int32), ("item_bytes", C.c_int32),
-                ("rem_packets", C.c_int64), ("rem_long_pieces", C.c_int64),
-                ("n_chunks", C.c_int64), ("n_bundles", C.c_int64), ("stream_bytes", C.c_int64),
-                ("n_bundle_lanes", C.c_int64),
-                ("arch", C.c_int32), ("unit_staged", C.c_int32), ("n_units", C.c_int64),
+                ("exec_grid", C.c_int32), ("unit_bytes", C.c_int32), ("n_units", C.c_int64),
                 ("n_unit_batches", C.c_int64), ("n_combine", C.c_int64),
                 ("panel_elems", C.c_int64), ("xmap_entries", C.c_int64)]
 
@@ -101,6 +96,8 @@ _sig = {
     "sable_serialize": [_H, _P, C.c_int64, C.POINTER(C.c_int64)],
     "sable_spmm": [_H, _P, _P, C.c_int32, _P],
     "sable_deserialize": [_P, C.c_int64, _P, C.POINTER(_H)],
+    "sable_comm_check": [_H],
+    "sable_exchange_rows": [_P, C.c_int32, _P, C.c_int32, _P],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -166,6 +163,20 @@ def sable_shard_bounds(weights, world: int) -> np.ndarray:
     _check(_lib.sable_shard_bounds(_P(w.ctypes.data), len(w), world, _P(b.ctypes.data)),
            "sable_shard_bounds")
     return b
+
+
+def sable_exchange_rows(weights, rpntr, world: int) -> np.ndarray:
+    """Global row bounds of every rank's slice of y in the all-gather (host)."""
+    w = np.ascontiguousarray(weights, dtype=np.int64)
+    rp = np.ascontiguousarray(rpntr, dtype=np.int32)
+    out = np.zeros(world + 1, dtype=np.int64)
+    _check(_lib.sable_exchange_rows(_P(w.ctypes.data), len(w), _P(rp.ctypes.data), world,
+                                    _P(out.ctypes.data)), "sable_exchange_rows")
+    return out
+
+
+def sable_comm_check(h: int) -> None:
+    _check(_lib.sable_comm_check(_H(h)), "sable_comm_check")
 
 
 def sable_nccl_unique_id() -> bytes:
@@ -265,12 +276,19 @@ class VbrMatrix:
         first = arrays["val"]
         on_dev = isinstance(first, torch.Tensor) and first.is_cuda
 
+        tdt = {np.int32: torch.int32, np.int64: torch.int64, np.float32: torch.float32,
+               np.float64: torch.float64}
+
         def ptr(name, dt):
             a = arrays.get(name)
             if a is None:
                 return None, 0
             if on_dev:
-                t = a.contiguous()
+                # every array in its ABI dtype on this handle's device (a
+                # wrong width would be read as another type by the library)
+                if not (isinstance(a, torch.Tensor) and a.is_cuda):
+                    raise TypeError(f"{name}: all arrays must be CUDA tensors when val is")
+                t = a.to(device=self.device, dtype=tdt[dt]).contiguous()
                 keep.append(t)
                 return t.data_ptr(), t.numel()
             n = np.ascontiguousarray(a, dtype=dt)
@@ -339,6 +357,9 @@ class VbrMatrix:
 
     def comm_init(self, uid: bytes):
         sable_comm_init(self.handle, uid)
+
+    def comm_check(self):
+        sable_comm_check(self.handle)
 
     def spmv_allgather(self, x, x_next, stream=None):
         import torch

@@ -61,6 +61,10 @@ def _worker(rank, world, port, out):
         dist.all_gather(allb, torch.from_numpy(bounds.astype(np.int32)))
         same = all(torch.equal(b, allb[0]) for b in allb)
         ranges = sdist.row_ranges(s.rpntr, bounds)
+        # the rows libsable.so's all-gather broadcasts for every rank
+        # (sable_exchange_rows: the host layout comm.cu follows)
+        ex = sdist.sable.sable_exchange_rows(weights, s.rpntr, world)
+        layout_ok = [(int(ex[q]), int(ex[q + 1])) for q in range(world)] == ranges
         r0, r1 = ranges[rank]
         rp = s.rowptr()
         x = s.x.astype(np.float64)
@@ -76,7 +80,7 @@ def _worker(rank, world, port, out):
             x = np.concatenate([g[:n].numpy() for g, n in zip(gathered, sizes)])
             xs.append(x)
         if rank == 0:
-            out.put((same, bounds.tolist(), ranges, [v.tolist() for v in xs]))
+            out.put((same and layout_ok, bounds.tolist(), ranges, [v.tolist() for v in xs]))
     finally:
         dist.destroy_process_group()
 
@@ -92,7 +96,7 @@ def test_sharded_iteration_matches_oracle(world):
     same, bounds, ranges, xs = q.get(timeout=240)  # before join: the queue must drain
     while not pc.join():
         pass
-    assert same, "ranks derived different shard bounds"
+    assert same, "ranks derived different shard bounds or exchange rows"
     s, area, rem_per_row = _case()
     nbr = len(s.rpntr) - 1
     assert bounds[0] == 0 and bounds[-1] == nbr and all(a <= b for a, b in zip(bounds, bounds[1:]))

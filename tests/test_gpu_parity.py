@@ -384,21 +384,13 @@ def test_comm_world1(sable):
 # ------------------------------------------------------------------ executor shapes
 
 EXEC_CFGS = {
-    # the unit executor (arch 2, the default): direct loads, and the staged
-    # variant (bulk copies through two shared-memory stages per warp)
     "unit": {},
-    "unit_staged": dict(SABLE_UNIT_STAGED=1),
     # tiny unit budget: remainders cut into many pieces, wide panels cut into
     # column chunks, few rows per remainder unit, one unit per warp
     "unit_small": dict(SABLE_USTAGE=1024, SABLE_UREM_ROWS=3, SABLE_UBATCH_UNITS=1),
-    "unit_staged_small": dict(SABLE_UNIT_STAGED=1, SABLE_USTAGE=1024, SABLE_UBATCH_UNITS=7),
+    "unit_mid": dict(SABLE_USTAGE=4096, SABLE_UBATCH_UNITS=7),
     # long warp batches, no L2 prefetch
     "unit_long_batches": dict(SABLE_UBATCH_UNITS=64, SABLE_XPREFETCH=0),
-    # the legacy stream executors (arch 0 / 1), kept for A/B measurement
-    "legacy_warp": dict(SABLE_ARCH=0, SABLE_STAGE_BYTES=1024, SABLE_ITEM_BYTES=64, SABLE_NSTAGE=2,
-                        SABLE_XBUF=64, SABLE_TASKS=997),
-    "legacy_cta": dict(SABLE_ARCH=1, SABLE_STAGE_BYTES=2048, SABLE_NSTAGE=3, SABLE_ITEM_BYTES=256,
-                       SABLE_TASKS=37),
 }
 
 
@@ -418,15 +410,14 @@ def test_executor_configurations(sable, monkeypatch, cfg):
     for s in cases:
         for split in ("rect", "all_rem"):
             A, _ = check(sable, s, split, exact=s.name in ("rand23", "longrows"))
-            if "SABLE_TASKS" in EXEC_CFGS[cfg]:
-                assert A.info["n_tasks"] == EXEC_CFGS[cfg]["SABLE_TASKS"]
             A.close()
 
 
-@pytest.mark.parametrize("env", [dict(SABLE_ITEM_BYTES=8), dict(SABLE_USTAGE=1000),
-                                 dict(SABLE_ARCH=3)])
+@pytest.mark.parametrize("env", [dict(SABLE_USTAGE=512), dict(SABLE_USTAGE=1000),
+                                 dict(SABLE_ARCH=1), dict(SABLE_UREM_ROWS=33),
+                                 dict(SABLE_UBATCH_UNITS=0)])
 def test_executor_config_rejected(sable, monkeypatch, env):
-    for k, v in env.items():  # below one value per row / not 16-aligned / no such arch
+    for k, v in env.items():  # below the minimum / not 16-aligned / no such executor
         monkeypatch.setenv(k, str(v))
     s = gen.make("c1")
     with pytest.raises(sable.SableError) as e:

@@ -95,3 +95,38 @@ def test_suitability_survives(sable):
     assert A.info["suitable"] == B.info["suitable"] == 0
     A.close()
     B.close()
+
+
+def _fnv1a(b: bytes) -> int:
+    h = 1469598103934665603
+    for c in b:
+        h ^= c
+        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def test_image_semantic_checks(sable):
+    """An image whose checksum is right but whose content is not (a header
+    field out of range, or a unit index past its arrays, with the payload
+    checksum recomputed) is rejected with SABLE_E_FORMAT before any upload."""
+    import struct
+    s = gen.make("c1")
+    A = make(sable, s)
+    img = bytes(A.serialize())
+    A.close()
+    hdr = struct.unpack_from("<i", img, 12)[0]
+    assert hdr == 416  # ImageHeader layout of serial.cu
+    # executor configuration: rem_rows (cfg at byte 96: pf, ustage, rem_rows, batch)
+    bad = bytearray(img)
+    struct.pack_into("<i", bad, 104, 99)
+    with pytest.raises(sable.SableError) as e:
+        sable.VbrMatrix.from_image(bytes(bad))
+    assert e.value.status == sable.SABLE_E_FORMAT
+    # unit 0 (section 0, right after the header): rows past the local rows
+    bad = bytearray(img)
+    struct.pack_into("<i", bad, hdr + 4, 1 << 30)  # row0
+    struct.pack_into("<Q", bad, 248, _fnv1a(bytes(bad[hdr:])))
+    with pytest.raises(sable.SableError) as e:
+        sable.VbrMatrix.from_image(bytes(bad))
+    assert e.value.status == sable.SABLE_E_FORMAT
+    assert "unit 0" in str(e.value)
