@@ -59,6 +59,11 @@ def _load():
         lib.oracle_partition.argtypes = [C.c_int64, C.c_int64, C.c_int64, P, P, P,
                                          C.c_int32, P, C.c_int32, P, C.c_int32,
                                          C.c_int32, C.c_int32, C.POINTER(C.c_int)]
+        lib.oracle_partition_policy.restype = C.POINTER(_Partition)
+        lib.oracle_partition_policy.argtypes = [C.c_int64, C.c_int64, C.c_int64, P, P, P,
+                                                C.c_int32, P, C.c_int32, P, C.c_int32,
+                                                C.c_int64, C.c_int32, P, C.c_int32,
+                                                C.c_int32, C.POINTER(C.c_int)]
         lib.oracle_partition_free.restype = None
         lib.oracle_partition_free.argtypes = [C.POINTER(_Partition)]
         lib.oracle_spmv.restype = None
@@ -104,8 +109,12 @@ def _arr(ptr, n, dtype):
 
 
 def partition(nrows: int, ncols: int, I, J, V, rpntr, cpntr, delta: int,
-              a0: int = 0, a1: int | None = None) -> dict:
+              a0: int = 0, a1: int | None = None, min_area: int = 0, rules=None) -> dict:
     """SURVEY 8(c) steps 3-6 over block rows [a0, a1) of normalised COO.
+
+    min_area / rules: the per-shape delta policy (reading R22): rules is a
+    sequence of (h_min, h_max, w_min, w_max, delta), the first match wins;
+    `delta` is the default for unmatched shapes.
 
     Returns the canonical export: cell_br, cell_bc,
     cell_cnt, cell_dense, tile_off, tile_val (float64), ublocks, rem_indptr,
@@ -121,8 +130,15 @@ def partition(nrows: int, ncols: int, I, J, V, rpntr, cpntr, delta: int,
     if a1 is None:
         a1 = nbr
     err = C.c_int(0)
-    res = lib.oracle_partition(nrows, ncols, len(I), _p(I), _p(J), _p(V), nbr, _p(rp),
-                               nbc, _p(cp), int(delta), int(a0), int(a1), C.byref(err))
+    if min_area or rules:
+        rr = _c(np.asarray(rules if rules else np.zeros((0, 5)), np.int64).reshape(-1, 5),
+                np.int32)
+        res = lib.oracle_partition_policy(nrows, ncols, len(I), _p(I), _p(J), _p(V), nbr,
+                                          _p(rp), nbc, _p(cp), int(delta), int(min_area),
+                                          len(rr), _p(rr), int(a0), int(a1), C.byref(err))
+    else:
+        res = lib.oracle_partition(nrows, ncols, len(I), _p(I), _p(J), _p(V), nbr, _p(rp),
+                                   nbc, _p(cp), int(delta), int(a0), int(a1), C.byref(err))
     if not res:
         raise OracleError(_ERRS.get(err.value, str(err.value)))
     try:

@@ -202,10 +202,39 @@ static int32_t count_block_row(int64_t k0, int64_t k1, const int64_t *J,
   return nt;
 }
 
-/* Step 5: the delta-dense rule, in integers. */
-static int is_dense(int64_t cnt, int64_t h, int64_t w, int32_t delta) {
-  return 100 * cnt >= (int64_t)delta * h * w;
+/* Step 5: the delta-dense rule, in integers.  With a
+ * per-shape policy (reading R22: the B200
+ * replacement of the paper's per-block classifier):
+ * a cell of h x w is dense iff h*w >= min_area and
+ * 100*cnt >= delta(h, w)*h*w, where delta(h, w) is the delta of the first
+ * rule with h_min <= h <= h_max and w_min <= w <= w_max, else the default.
+ * rules holds n_rules records of 5 int32: h_min, h_max, w_min, w_max, delta. */
+typedef struct {
+  int32_t delta;
+  int64_t min_area;
+  int32_t n_rules;
+  const int32_t *rules;
+} policy_t;
+
+static int32_t delta_for(const policy_t *pol, int64_t h, int64_t w) {
+  for (int32_t k = 0; k < pol->n_rules; ++k) {
+    const int32_t *r = pol->rules + 5 * k;
+    if (h >= r[0] && h <= r[1] && w >= r[2] && w <= r[3]) return r[4];
+  }
+  return pol->delta;
 }
+
+static int is_dense(int64_t cnt, int64_t h, int64_t w, const policy_t *pol) {
+  if (h * w < pol->min_area) return 0;
+  return 100 * cnt >= (int64_t)delta_for(pol, h, w) * h * w;
+}
+
+static oracle_partition_t *partition_impl(int64_t nrows, int64_t ncols, int64_t nnz,
+                                          const int64_t *I, const int64_t *J,
+                                          const double *V, int32_t nbr,
+                                          const int32_t *rpntr, int32_t nbc,
+                                          const int32_t *cpntr, const policy_t *pol,
+                                          int32_t a0, int32_t a1, int *err);
 
 oracle_partition_t *oracle_partition(int64_t nrows, int64_t ncols, int64_t nnz,
                                      const int64_t *I, const int64_t *J,
@@ -213,7 +242,41 @@ oracle_partition_t *oracle_partition(int64_t nrows, int64_t ncols, int64_t nnz,
                                      const int32_t *rpntr, int32_t nbc,
                                      const int32_t *cpntr, int32_t delta,
                                      int32_t a0, int32_t a1, int *err) {
+  const policy_t pol = {delta, 0, 0, NULL};
+  return partition_impl(nrows, ncols, nnz, I, J, V, nbr, rpntr, nbc, cpntr, &pol, a0, a1, err);
+}
+
+/* The same partition under a per-shape policy (see is_dense). */
+oracle_partition_t *oracle_partition_policy(int64_t nrows, int64_t ncols, int64_t nnz,
+                                            const int64_t *I, const int64_t *J,
+                                            const double *V, int32_t nbr,
+                                            const int32_t *rpntr, int32_t nbc,
+                                            const int32_t *cpntr, int32_t delta,
+                                            int64_t min_area, int32_t n_rules,
+                                            const int32_t *rules, int32_t a0, int32_t a1,
+                                            int *err) {
   *err = OR_OK;
+  if (min_area < 0 || n_rules < 0 || (n_rules > 0 && !rules)) {
+    *err = OR_E_ARG;
+    return NULL;
+  }
+  for (int32_t k = 0; k < n_rules; ++k)
+    if (rules[5 * k + 4] < 0 || rules[5 * k + 4] > 101) {
+      *err = OR_E_ARG;
+      return NULL;
+    }
+  const policy_t pol = {delta, min_area, n_rules, rules};
+  return partition_impl(nrows, ncols, nnz, I, J, V, nbr, rpntr, nbc, cpntr, &pol, a0, a1, err);
+}
+
+static oracle_partition_t *partition_impl(int64_t nrows, int64_t ncols, int64_t nnz,
+                                          const int64_t *I, const int64_t *J,
+                                          const double *V, int32_t nbr,
+                                          const int32_t *rpntr, int32_t nbc,
+                                          const int32_t *cpntr, const policy_t *pol,
+                                          int32_t a0, int32_t a1, int *err) {
+  *err = OR_OK;
+  const int32_t delta = pol->delta;
   if (delta < 0 || delta > 101 || a0 < 0 || a1 > nbr || a0 > a1) {
     *err = OR_E_ARG;
     return NULL;
@@ -249,7 +312,7 @@ oracle_partition_t *oracle_partition(int64_t nrows, int64_t ncols, int64_t nnz,
       const int32_t b = touched[t];
       const int64_t w = cpntr[b + 1] - cpntr[b];
       p->n_cells++;
-      if (is_dense(cnt[b], h, w, delta)) {
+      if (is_dense(cnt[b], h, w, pol)) {
         p->n_dense++;
         p->tile_elems += h * w;
       } else {
@@ -285,7 +348,7 @@ oracle_partition_t *oracle_partition(int64_t nrows, int64_t ncols, int64_t nnz,
     for (int32_t t = 0; t < nt; ++t) {
       const int32_t b = touched[t];
       const int64_t w = cpntr[b + 1] - cpntr[b];
-      const int dense = is_dense(cnt[b], h, w, delta);
+      const int dense = is_dense(cnt[b], h, w, pol);
       p->cell_br[c_i] = a;
       p->cell_bc[c_i] = b;
       p->cell_cnt[c_i] = cnt[b];

@@ -56,19 +56,23 @@ constexpr int kUnitThreads = kUnitWarps * 32;
 #endif
 constexpr int kUnitMinBlocks = SABLE_UNIT_MINW / kUnitWarps;
 
-// Lane 0: pull a unit's data (dense rows, x map, remainder row pointers,
-// columns and values) into L2 while the previous unit computes, so the
-// unit's own loads wait on L2 rather than HBM.
+// Lane 0: pull a warp batch's data past its first unit into L2 with five
+// bulk prefetches -- the units of a batch are consecutive, so their panel
+// rows, x maps, remainder row pointers, columns and values are contiguous
+// ranges from the first unit's to the last unit's -- so the later units'
+// loads wait on L2 rather than HBM.
 template <typename T>
-__device__ __forceinline__ void prefetch_unit(const UPlan<T>& P, const Unit& U) {
-  if (U.wq > 0) {
-    l2_prefetch(reinterpret_cast<const uint4*>(P.pv) + U.voff16, (int64_t)U.nr * U.wq * 16);
-    l2_prefetch(P.xq + U.xq0, (int64_t)U.wq * 4);
-  }
-  if (U.e1 > U.e0) {
-    l2_prefetch(P.rptr + U.row0, (int64_t)(U.nr + 1) * 4);
-    l2_prefetch(P.ridx + U.e0, (int64_t)(U.e1 - U.e0) * 4);
-    l2_prefetch(P.rval + U.e0, (int64_t)(U.e1 - U.e0) * sizeof(T));
+__device__ __forceinline__ void prefetch_span(const UPlan<T>& P, const Unit& A, const Unit& B) {
+  const int64_t v0 = A.wq > 0 ? A.voff16 : B.voff16;
+  const int64_t v1 = B.wq > 0 ? (int64_t)B.voff16 + (int64_t)B.nr * B.wq : (int64_t)A.voff16;
+  if (v1 > v0) l2_prefetch(reinterpret_cast<const uint4*>(P.pv) + v0, (v1 - v0) * 16);
+  const int64_t q0 = A.wq > 0 ? A.xq0 : B.xq0;
+  const int64_t q1 = B.wq > 0 ? (int64_t)B.xq0 + B.wq : (int64_t)A.xq0;
+  if (q1 > q0) l2_prefetch(P.xq + q0, (q1 - q0) * 4);
+  l2_prefetch(P.rptr + A.row0, ((int64_t)B.row0 + B.nr + 1 - A.row0) * 4);
+  if (B.e1 > A.e0) {
+    l2_prefetch(P.ridx + A.e0, (int64_t)(B.e1 - A.e0) * 4);
+    l2_prefetch(P.rval + A.e0, (int64_t)(B.e1 - A.e0) * sizeof(T));
   }
 }
 
@@ -210,15 +214,49 @@ __device__ __forceinline__ void rem_load(const UPlan<T>& P, int c0, int e1, int 
   }
 }
 
+// A remainder of at most 32 entries (most units that also have dense rows):
+// one entry per lane (its column and value loaded before the dense part),
+// the products summed per row by a segmented inclusive scan over the lanes
+// (Hillis-Steele with row-head flags: a fixed tree per row), and row r's sum
+// taken from the lane of its last entry -- no shared memory, no barrier.
+template <typename T, int KV>
+__device__ __forceinline__ void rem_small(const Unit& U, const T* __restrict__ x, int lane,
+                                          int c, T v, int lo, int hi, T (&s)[KV]) {
+  const int n = U.e1 - U.e0;
+  T p[KV];
+  {
+    T xg[KV];
+#pragma unroll
+    for (int j = 0; j < KV; ++j) xg[j] = T(0);
+    if (lane < n) ldg_kv<T, KV>(x + (int64_t)c * KV, xg);
+#pragma unroll
+    for (int j = 0; j < KV; ++j) p[j] = v * xg[j];
+  }
+  const bool row = lane < U.nr && hi > lo;
+  const unsigned heads = __reduce_or_sync(kFull, row ? 1u << (lo - U.e0) : 0u) | 1u;
+  bool f = (heads >> lane) & 1u;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const bool ft = __shfl_up_sync(kFull, f, o);
+#pragma unroll
+    for (int j = 0; j < KV; ++j) {
+      const T t = __shfl_up_sync(kFull, p[j], o);
+      if (lane >= o && !f) p[j] += t;
+    }
+    if (lane >= o) f = f || ft;
+  }
+  const int src = row ? hi - 1 - U.e0 : 0;
+#pragma unroll
+  for (int j = 0; j < KV; ++j) {
+    const T t = __shfl_sync(kFull, p[j], src);
+    if (row) s[j] += t;
+  }
+}
+
 template <typename T, int KV>
 __device__ __forceinline__ void rem_rows(const UPlan<T>& P, const Unit& U,
-                                         const T* __restrict__ x, T* buf, int lane,
-                                         T (&s)[KV]) {
-  int lo = 0, hi = 0;
-  if (lane < U.nr) {
-    lo = max(__ldg(P.rptr + U.row0 + lane), U.e0);
-    hi = min(__ldg(P.rptr + U.row0 + lane + 1), U.e1);
-  }
+                                         const T* __restrict__ x, T* buf, int lane, int lo,
+                                         int hi, T (&s)[KV]) {
   RemWave<T> w;
   rem_load(P, U.e0, U.e1, lane, w);
 #pragma unroll 1
@@ -243,10 +281,25 @@ __device__ __forceinline__ void rem_rows(const UPlan<T>& P, const Unit& U,
     __syncwarp();
     const int a = max(lo, c0) - c0, b = min(hi, c0 + n) - c0;
     const bool longr = b - a > 32;
-    if (!longr)
-      for (int e = a; e < b; ++e)
+    if (!longr) {
+      // four interleaved partial sums (entries e = a + 4i + m go to m), added
+      // in a fixed order: a short dependence chain, an order fixed by the row
 #pragma unroll
-        for (int j = 0; j < KV; ++j) s[j] += buf[e * KV + j];
+      for (int j = 0; j < KV; ++j) {
+        T q0 = T(0), q1 = T(0), q2 = T(0), q3 = T(0);
+        int e = a;
+        for (; e + 3 < b; e += 4) {
+          q0 += buf[e * KV + j];
+          q1 += buf[(e + 1) * KV + j];
+          q2 += buf[(e + 2) * KV + j];
+          q3 += buf[(e + 3) * KV + j];
+        }
+        if (e < b) q0 += buf[e * KV + j];
+        if (e + 1 < b) q1 += buf[(e + 1) * KV + j];
+        if (e + 2 < b) q2 += buf[(e + 2) * KV + j];
+        s[j] += (q0 + q1) + (q2 + q3);
+      }
+    }
     unsigned lm = __ballot_sync(kFull, longr);
     while (lm) {
       const int q = __ffs(lm) - 1;
@@ -308,14 +361,34 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
   const int64_t b = P.b0 + (int64_t)blockIdx.x * kUnitWarps + warp;
   if (b >= P.n_batches) return;
   const int u0 = __ldg(P.batch + b), u1 = __ldg(P.batch + b + 1);
-  if (lane == 0 && P.pf) l2_prefetch(P.units + u0, (int64_t)(u1 - u0) * sizeof(Unit));
   Unit Un = load_unit(P.units + u0);
+  if (P.pf && u1 - u0 > 1) {
+    // the batch's data past its first unit -- contiguous ranges of the
+    // panels, x maps, remainder pointers, columns and values -- into L2
+    const Unit Ul = load_unit(P.units + u1 - 1);
+    if (lane == 0) prefetch_span<T>(P, Un, Ul);
+  }
   for (int u = u0; u < u1; ++u) {
     const Unit U = Un;
     if (u + 1 < u1) Un = load_unit(P.units + u + 1);
     T s[KV];
 #pragma unroll
     for (int j = 0; j < KV; ++j) s[j] = T(0);
+    // remainder row bounds, and a short remainder's entries, in flight
+    // during the dense part
+    const int ne = U.e1 - U.e0;
+    int lo = 0, hi = 0, rc = 0;
+    T rv = T(0);
+    if (ne > 0) {
+      if (lane < U.nr) {
+        lo = max(__ldg(P.rptr + U.row0 + lane), U.e0);
+        hi = min(__ldg(P.rptr + U.row0 + lane + 1), U.e1);
+      }
+      if (ne <= 32 && lane < ne) {
+        rc = __ldcs(P.ridx + U.e0 + lane);
+        rv = __ldcs(P.rval + U.e0 + lane);
+      }
+    }
     if (U.wq > 0) {
       switch (U.llpr) {
         case 0: dense_rows<T, 1, KV>(P, U, x, lane, s); break;
@@ -326,8 +399,10 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
         default: dense_rows<T, 32, KV>(P, U, x, lane, s); break;
       }
     }
-    if (lane == 0 && P.pf && u + 1 < u1) prefetch_unit(P, Un);
-    if (U.e1 > U.e0) rem_rows<T, KV>(P, U, x, buf_s[warp], lane, s);
+    if (ne > 0 && ne <= 32)
+      rem_small<T, KV>(U, x, lane, rc, rv, lo, hi, s);
+    else if (ne > 0)
+      rem_rows<T, KV>(P, U, x, buf_s[warp], lane, lo, hi, s);
     finish_unit<T, KV>(P, U, s, y, lane);
   }
 }

@@ -115,7 +115,7 @@ def test_image_semantic_checks(sable):
     img = bytes(A.serialize())
     A.close()
     hdr = struct.unpack_from("<i", img, 12)[0]
-    assert hdr == 416  # ImageHeader layout of serial.cu
+    fnv_at = hdr - 8 * 22 - 8  # ImageHeader of serial.cu: ..., payload_fnv, section_bytes[22]
     # executor configuration: rem_rows (cfg at byte 96: pf, ustage, rem_rows, batch)
     bad = bytearray(img)
     struct.pack_into("<i", bad, 104, 99)
@@ -125,7 +125,7 @@ def test_image_semantic_checks(sable):
     # unit 0 (section 0, right after the header): rows past the local rows
     bad = bytearray(img)
     struct.pack_into("<i", bad, hdr + 4, 1 << 30)  # row0
-    struct.pack_into("<Q", bad, 248, _fnv1a(bytes(bad[hdr:])))
+    struct.pack_into("<Q", bad, fnv_at, _fnv1a(bytes(bad[hdr:])))
     with pytest.raises(sable.SableError) as e:
         sable.VbrMatrix.from_image(bytes(bad))
     assert e.value.status == sable.SABLE_E_FORMAT

@@ -20,8 +20,10 @@ from golden_io import coo, load
 # ---------------------------------------------------------------- helpers
 
 
-def brute_partition(A, rpntr, cpntr, delta):
-    """The partition by definition, on a dense matrix: slice every grid cell."""
+def brute_partition(A, rpntr, cpntr, delta, min_area=0, rules=()):
+    """The partition by definition, on a dense matrix: slice every grid cell.
+    min_area / rules: the per-shape policy of reading R22 (first matching
+    (h_min, h_max, w_min, w_max, delta) rule, else `delta`)."""
     cells, tiles, offs, ub = [], [], [0], []
     mask_rem = np.zeros(A.shape, dtype=bool)
     for a in range(len(rpntr) - 1):
@@ -31,7 +33,8 @@ def brute_partition(A, rpntr, cpntr, delta):
             if cnt == 0:
                 continue
             h, w = sub.shape
-            dense = cnt * 100 >= delta * h * w
+            d = next((r[4] for r in rules if r[0] <= h <= r[1] and r[2] <= w <= r[3]), delta)
+            dense = h * w >= min_area and cnt * 100 >= d * h * w
             if dense:
                 tiles.append(sub.flatten(order="F"))
                 offs.append(offs[-1] + h * w)
@@ -49,9 +52,10 @@ def brute_partition(A, rpntr, cpntr, delta):
         rem_val=R.data)
 
 
-def run(A, rpntr, cpntr, delta, a0=0, a1=None):
+def run(A, rpntr, cpntr, delta, a0=0, a1=None, min_area=0, rules=None):
     I, J, V = coo(A)
-    return oracle.partition(A.shape[0], A.shape[1], I, J, V, rpntr, cpntr, delta, a0, a1)
+    return oracle.partition(A.shape[0], A.shape[1], I, J, V, rpntr, cpntr, delta, a0, a1,
+                            min_area=min_area, rules=rules)
 
 
 def cells_of(p):
@@ -360,3 +364,58 @@ def test_spmv_rows_sample_equals_full():
     ys, ss = oracle.spmv_rows(oracle.rowptr(50, I), J, V, x, rows)
     np.testing.assert_array_equal(ys, y[rows])
     np.testing.assert_array_equal(ss, s[rows])
+
+
+# ------------------------------------------------- per-shape delta policy (f2)
+
+
+def random_rules(g, k):
+    rules = []
+    for _ in range(k):
+        h0, w0 = int(g.integers(1, 6)), int(g.integers(1, 6))
+        rules.append((h0, h0 + int(g.integers(0, 6)), w0, w0 + int(g.integers(0, 6)),
+                      int(g.choice([0, 25, 50, 67, 80, 101]))))
+    return rules
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_policy_matches_brute_force(seed):
+    """Reading R22 on random grids: the first matching shape rule's delta,
+    min_area, cell counts by slicing the dense matrix."""
+    g = np.random.default_rng(100 + seed)
+    A, rp, cp = random_case(100 + seed, 40, 37, 9, 8)
+    rules = random_rules(g, int(g.integers(1, 5)))
+    min_area = int(g.choice([0, 1, 4, 9, 30]))
+    delta = int(g.choice([0, 50, 75, 101]))
+    assert_same(run(A, rp, cp, delta, min_area=min_area, rules=rules),
+                brute_partition(A, rp, cp, delta, min_area, rules))
+
+
+@pytest.mark.parametrize("delta", [0, 50, 67, 101])
+def test_policy_special_cases(delta):
+    A, rp, cp = random_case(7, 50, 45, 10, 9)
+    plain = run(A, rp, cp, delta)
+    # a rule over every shape, or min_area 1 with no rule: the plain delta rule
+    assert_same(run(A, rp, cp, 3, rules=[(1, 50, 1, 45, delta)]), brute_partition(A, rp, cp, delta))
+    assert_same(run(A, rp, cp, delta, min_area=1), brute_partition(A, rp, cp, delta))
+    for k in ("cell_dense", "tile_val", "rem_indices"):
+        np.testing.assert_array_equal(run(A, rp, cp, delta, min_area=1)[k], plain[k])
+    # min_area above every cell: nothing dense, the remainder is the input CSR
+    big = run(A, rp, cp, delta, min_area=50 * 45 + 1)
+    assert big["n_dense"] == 0
+    R = sp.csr_matrix(A)
+    np.testing.assert_array_equal(big["rem_indptr"], R.indptr)
+    np.testing.assert_array_equal(big["rem_indices"], R.indices)
+
+
+def test_policy_first_rule_wins_and_monotone():
+    A, rp, cp = random_case(8, 60, 60, 12, 12)
+    r_lo = [(1, 60, 1, 60, 30)]
+    r_hi = [(1, 60, 1, 60, 90)]
+    lo = run(A, rp, cp, 50, rules=r_lo + r_hi)
+    assert_same(lo, brute_partition(A, rp, cp, 30))
+    hi = run(A, rp, cp, 50, rules=r_hi + r_lo)
+    assert_same(hi, brute_partition(A, rp, cp, 90))
+    # delta-monotone under a policy too: raising every rule's delta keeps a subset dense
+    d_lo, d_hi = lo["cell_dense"].astype(bool), hi["cell_dense"].astype(bool)
+    assert np.all(d_hi <= d_lo)
