@@ -195,6 +195,33 @@ sable_status sable_spmv(sable_handle* h, const void* x, void* y, void* cuda_stre
 sable_status sable_spmv_host(sable_handle* h, const void* x_host, void* y_host,
                              void* cuda_stream);
 
+/* ---- per-shape delta policy (reading R22) --
+ * The paper decides dense vs sparse per block with a model trained on its
+ * CPU's timings; here a measured B200 policy can replace
+ * the single delta: a candidate cell of h x w is dense iff h*w >= min_area
+ * and 100*cnt >= delta(h, w)*h*w, delta(h, w) = the delta of the FIRST rule
+ * with h_min <= h <= h_max and w_min <= w <= w_max, else delta_pct.  With
+ * no rules and min_area <= 1 this is sable_vbr_create's rule exactly.
+ * scripts/calibrate.py measures a policy (profiles/r02_f2_policy.json). */
+typedef struct {
+  int32_t h_min, h_max;  /* inclusive block-height range */
+  int32_t w_min, w_max;  /* inclusive block-width range  */
+  uint32_t delta_pct;    /* 0..101 for cells of these shapes */
+} sable_delta_rule;
+
+typedef struct {
+  uint32_t delta_pct;            /* cells matched by no rule, 0..101 */
+  int64_t min_area;              /* cells with h*w < min_area are never dense (>= 0) */
+  int32_t n_rules;               /* 0..64 */
+  const sable_delta_rule* rules; /* host memory, n_rules records */
+} sable_delta_policy;
+
+/* sable_vbr_create under a per-shape policy (SABLE_E_INVALID_ARG for a delta
+ * outside 0..101, a negative min_area or more than 64 rules). */
+sable_status sable_vbr_create_policy(const sable_vbr_desc* desc, const sable_delta_policy* policy,
+                                     const sable_shard* shard, void* cuda_stream,
+                                     sable_handle** out);
+
 /* Free the handle (NULL is a no-op).  Synchronises the device first. */
 sable_status sable_destroy(sable_handle* h);
 

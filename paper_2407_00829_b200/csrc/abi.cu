@@ -26,8 +26,8 @@ std::string cuda_msg(cudaError_t e, const char* what) {
   return std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
 }
 
-sable_status create_impl(const sable_vbr_desc* d, uint32_t delta, const sable_shard* sh,
-                         cudaStream_t st, sable_handle** out);
+sable_status create_impl(const sable_vbr_desc* d, const sable_delta_policy* pol,
+                         const sable_shard* sh, cudaStream_t st, sable_handle** out);
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st);
 cudaError_t run_spmm(const sable_handle* h, const void* X, void* Y, int32_t k, void* scratch,
                      cudaStream_t st);
@@ -159,11 +159,17 @@ sable_status sable_shard_bounds(const int64_t* weights, int32_t nbrows, int32_t 
   return SABLE_OK;
 }
 
-sable_status sable_vbr_create(const sable_vbr_desc* d, uint32_t delta_pct,
-                              const sable_shard* shard, void* cuda_stream, sable_handle** out) {
+sable_status sable_vbr_create_policy(const sable_vbr_desc* d, const sable_delta_policy* pol,
+                                     const sable_shard* shard, void* cuda_stream,
+                                     sable_handle** out) {
   if (out) *out = nullptr;
-  if (!d || !out) return fail(SABLE_E_INVALID_ARG, "sable_vbr_create: NULL desc or out");
-  if (delta_pct > 101) return fail(SABLE_E_INVALID_ARG, "delta_pct must be in [0, 101]");
+  if (!d || !out || !pol) return fail(SABLE_E_INVALID_ARG, "sable_vbr_create: NULL desc, policy or out");
+  if (pol->delta_pct > 101) return fail(SABLE_E_INVALID_ARG, "delta_pct must be in [0, 101]");
+  if (pol->min_area < 0 || pol->n_rules < 0 || pol->n_rules > 64 || (pol->n_rules > 0 && !pol->rules))
+    return fail(SABLE_E_INVALID_ARG, "delta policy: min_area >= 0 and 0..64 rules");
+  for (int32_t k = 0; k < pol->n_rules; ++k)
+    if (pol->rules[k].delta_pct > 101)
+      return fail(SABLE_E_INVALID_ARG, "delta policy: rule delta must be in [0, 101]");
   if (d->dtype != SABLE_F32 && d->dtype != SABLE_F64)
     return fail(SABLE_E_INVALID_ARG, "dtype must be SABLE_F32 or SABLE_F64");
   if (d->mem != SABLE_MEM_HOST && d->mem != SABLE_MEM_DEVICE)
@@ -188,7 +194,13 @@ sable_status sable_vbr_create(const sable_vbr_desc* d, uint32_t delta_pct,
   if (sh.world < 1 || sh.rank < 0 || sh.rank >= sh.world)
     return fail(SABLE_E_INVALID_ARG, "shard: need 0 <= rank < world");
   set_error("");
-  return create_impl(d, delta_pct, &sh, static_cast<cudaStream_t>(cuda_stream), out);
+  return create_impl(d, pol, &sh, static_cast<cudaStream_t>(cuda_stream), out);
+}
+
+sable_status sable_vbr_create(const sable_vbr_desc* d, uint32_t delta_pct,
+                              const sable_shard* shard, void* cuda_stream, sable_handle** out) {
+  const sable_delta_policy pol{delta_pct, 0, 0, nullptr};
+  return sable_vbr_create_policy(d, &pol, shard, cuda_stream, out);
 }
 
 sable_status sable_spmv(sable_handle* h, const void* x, void* y, void* cuda_stream) {

@@ -267,7 +267,8 @@ template <typename T>
 __global__ void k_classify(const uint64_t* cell_key, const int64_t* cell_cnt,
                            const int32_t* cell_blk, const int64_t* cnt_vbr, int64_t n_cells,
                            int64_t nbc, const int32_t* rpntr, const int32_t* cpntr,
-                           int32_t delta, int32_t* cell_br, int32_t* cell_bc,
+                           int32_t delta, int64_t min_area, int32_t n_rules,
+                           const sable_delta_rule* rules, int32_t* cell_br, int32_t* cell_bc,
                            uint8_t* cell_dense, int32_t* br_ncell, int32_t* br_ndense,
                            int32_t* br_W, unsigned long long* br_area,
                            unsigned long long* br_rem, unsigned long long* br_vbrsparse) {
@@ -277,7 +278,15 @@ __global__ void k_classify(const uint64_t* cell_key, const int64_t* cell_cnt,
   const int32_t bc = (int32_t)(cell_key[c] % (uint64_t)nbc);
   const int64_t h = rpntr[br + 1] - rpntr[br], w = cpntr[bc + 1] - cpntr[bc];
   const int64_t cnt = cell_cnt[c];
-  const bool dense = 100 * cnt >= (int64_t)delta * h * w;
+  // PAPER.md:87-88 (readings R1, R3), under the per-shape policy (R22): the
+  // first rule matching h x w gives delta, cells below min_area are sparse
+  int32_t d = delta;
+  for (int32_t k = 0; k < n_rules; ++k)
+    if (h >= rules[k].h_min && h <= rules[k].h_max && w >= rules[k].w_min && w <= rules[k].w_max) {
+      d = (int32_t)rules[k].delta_pct;
+      break;
+    }
+  const bool dense = h * w >= min_area && 100 * cnt >= (int64_t)d * h * w;
   cell_br[c] = br;
   cell_bc[c] = bc;
   cell_dense[c] = dense ? 1 : 0;
@@ -546,8 +555,9 @@ ExecCfg exec_config() {
 // ------------------------------------------------------------------- inspect
 
 template <typename T>
-void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world,
+void inspect(const sable_vbr_desc* d, const sable_delta_policy* pol, int32_t rank, int32_t world,
              cudaStream_t st, sable_handle* h) {
+  const int32_t delta = (int32_t)pol->delta_pct;
   const int TH = 256;
   const int64_t nrows = d->nrows, ncols = d->ncols, nblk = d->nblocks, R = d->rem_nnz;
   const int32_t nbr = d->nbrows, nbc = d->nbcols;
@@ -680,11 +690,17 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
   int32_t* cell_br = cbr_b.as<int32_t>();
   int32_t* cell_bc = cbc_b.as<int32_t>();
   uint8_t* cell_dense = cden_b.as<uint8_t>();
+  DevBuf rules_b;
+  SB_CU(rules_b.alloc(sizeof(sable_delta_rule) * std::max<int32_t>(pol->n_rules, 1), st));
+  const sable_delta_rule* rules_d = rules_b.as<sable_delta_rule>();
+  if (pol->n_rules > 0)
+    SB_CU(cudaMemcpyAsync(rules_b.p, pol->rules, sizeof(sable_delta_rule) * pol->n_rules,
+                          cudaMemcpyHostToDevice, st));
   if (n_cells_all > 0)
     k_classify<T><<<nblocks_for(n_cells_all, TH), TH, 0, st>>>(
         ckey_b.as<uint64_t>(), cell_cnt, cell_blk, cnt_vbr, n_cells_all, nbc, in.rpntr,
-        in.cpntr, delta, cell_br, cell_bc, cell_dense, br_ncell, br_ndense, br_Wd, br_area,
-        br_rem, br_vsp);
+        in.cpntr, delta, pol->min_area, pol->n_rules, rules_d, cell_br, cell_bc, cell_dense,
+        br_ncell, br_ndense, br_Wd, br_area, br_rem, br_vsp);
   SB_CU(cudaGetLastError());
 
   std::vector<int32_t> H_ncell(nbr), H_ndense(nbr), H_W(nbr), H_rpntr(nbr + 1);
@@ -976,8 +992,8 @@ void inspect(const sable_vbr_desc* d, int32_t delta, int32_t rank, int32_t world
 
 }  // namespace
 
-sable_status create_impl(const sable_vbr_desc* d, uint32_t delta, const sable_shard* sh,
-                         cudaStream_t st, sable_handle** out) {
+sable_status create_impl(const sable_vbr_desc* d, const sable_delta_policy* pol,
+                         const sable_shard* sh, cudaStream_t st, sable_handle** out) {
   const auto t0 = std::chrono::steady_clock::now();
   sable_handle* h = new (std::nothrow) sable_handle();
   if (!h) {
@@ -985,7 +1001,7 @@ sable_status create_impl(const sable_vbr_desc* d, uint32_t delta, const sable_sh
     return SABLE_E_OOM;
   }
   h->dtype = d->dtype;
-  h->delta = (int32_t)delta;
+  h->delta = (int32_t)pol->delta_pct;
   h->nrows = d->nrows;
   h->ncols = d->ncols;
   h->nbr = d->nbrows;
@@ -995,9 +1011,9 @@ sable_status create_impl(const sable_vbr_desc* d, uint32_t delta, const sable_sh
   cudaGetDevice(&h->device);
   try {
     if (d->dtype == SABLE_F64)
-      inspect<double>(d, (int32_t)delta, h->rank, h->world, st, h);
+      inspect<double>(d, pol, h->rank, h->world, st, h);
     else
-      inspect<float>(d, (int32_t)delta, h->rank, h->world, st, h);
+      inspect<float>(d, pol, h->rank, h->world, st, h);
   } catch (const Fail& f) {
     cudaStreamSynchronize(st);
     free_handle(h);

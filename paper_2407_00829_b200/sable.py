@@ -36,7 +36,8 @@ EXPORTS = ("sable_vbr_create", "sable_spmv", "sable_spmv_host", "sable_destroy",
            "sable_nccl_unique_id", "sable_comm_init", "sable_spmv_allgather",
            "sable_spmv_iterate", "sable_status_string", "sable_last_error",
            "sable_abi_version", "sable_partition_grid", "sable_serialize",
-           "sable_deserialize", "sable_spmm", "sable_comm_check", "sable_exchange_rows")
+           "sable_deserialize", "sable_spmm", "sable_comm_check", "sable_exchange_rows",
+           "sable_vbr_create_policy")
 
 
 class sable_vbr_desc(C.Structure):
@@ -52,6 +53,16 @@ class sable_vbr_desc(C.Structure):
 
 class sable_shard(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32)]
+
+
+class sable_delta_rule(C.Structure):
+    _fields_ = [("h_min", C.c_int32), ("h_max", C.c_int32), ("w_min", C.c_int32),
+                ("w_max", C.c_int32), ("delta_pct", C.c_uint32)]
+
+
+class sable_delta_policy(C.Structure):
+    _fields_ = [("delta_pct", C.c_uint32), ("min_area", C.c_int64), ("n_rules", C.c_int32),
+                ("rules", C.POINTER(sable_delta_rule))]
 
 
 class sable_info(C.Structure):
@@ -97,6 +108,8 @@ _sig = {
     "sable_spmm": [_H, _P, _P, C.c_int32, _P],
     "sable_deserialize": [_P, C.c_int64, _P, C.POINTER(_H)],
     "sable_comm_check": [_H],
+    "sable_vbr_create_policy": [C.POINTER(sable_vbr_desc), C.POINTER(sable_delta_policy),
+                                C.POINTER(sable_shard), _P, C.POINTER(_H)],
     "sable_exchange_rows": [_P, C.c_int32, _P, C.c_int32, _P],
 }
 for _name, _args in _sig.items():
@@ -132,6 +145,19 @@ def sable_vbr_create(desc: sable_vbr_desc, delta_pct: int, rank: int = 0, world:
     sh = sable_shard(rank, world)
     _check(_lib.sable_vbr_create(C.byref(desc), delta_pct, C.byref(sh), _P(stream), C.byref(h)),
            "sable_vbr_create")
+    return h.value
+
+
+def sable_vbr_create_policy(desc: sable_vbr_desc, delta_pct: int, min_area: int = 0,
+                            rules=(), rank: int = 0, world: int = 1, stream: int = 0) -> int:
+    """sable_vbr_create under a per-shape delta policy: rules is a sequence
+    of (h_min, h_max, w_min, w_max, delta), the first match wins (R22)."""
+    h = _H()
+    sh = sable_shard(rank, world)
+    arr = (sable_delta_rule * max(1, len(rules)))(*[sable_delta_rule(*map(int, r)) for r in rules])
+    pol = sable_delta_policy(delta_pct, int(min_area), len(rules), arr)
+    _check(_lib.sable_vbr_create_policy(C.byref(desc), C.byref(pol), C.byref(sh), _P(stream),
+                                        C.byref(h)), "sable_vbr_create_policy")
     return h.value
 
 
@@ -269,7 +295,7 @@ class VbrMatrix:
     (numpy arrays or CUDA torch tensors, all of the same kind)."""
 
     def __init__(self, arrays: dict, nrows: int, ncols: int, delta: int = 50,
-                 rank: int = 0, world: int = 1, device=None):
+                 rank: int = 0, world: int = 1, device=None, policy: dict | None = None):
         import torch
         self.device = torch.device(device or "cuda")
         keep = []
@@ -315,7 +341,12 @@ class VbrMatrix:
         self.np_dtype = vdt
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream().cuda_stream
-            self.handle = sable_vbr_create(d, int(delta), rank, world, stream)
+            if policy:
+                self.handle = sable_vbr_create_policy(d, int(delta), policy.get("min_area", 0),
+                                                      policy.get("rules", ()), rank, world,
+                                                      stream)
+            else:
+                self.handle = sable_vbr_create(d, int(delta), rank, world, stream)
         self.info = sable_get_info(self.handle)
         del keep
 

@@ -423,3 +423,43 @@ def test_executor_config_rejected(sable, monkeypatch, env):
     with pytest.raises(sable.SableError) as e:
         handle(sable, s, "rect")
     assert e.value.status == sable.SABLE_E_INVALID_ARG
+
+
+# ------------------------------------------------------------------ per-shape delta policy
+
+@pytest.mark.parametrize("seed", range(6))
+def test_delta_policy(sable, seed):
+    """sable_vbr_create_policy (reading R22): the partition equals the
+    oracle's under the same rules and min_area, y within the tolerance."""
+    g = np.random.default_rng(500 + seed)
+    dt = np.float64 if seed % 2 else np.float32
+    s = gen.random_small(500 + seed, 400, 380, 40, 35, dtype=dt, density=0.3, dense_cells=0.5)
+    rules = []
+    for _ in range(int(g.integers(1, 5))):
+        h0, w0 = int(g.integers(1, 12)), int(g.integers(1, 12))
+        rules.append((h0, h0 + int(g.integers(0, 10)), w0, w0 + int(g.integers(0, 10)),
+                      int(g.choice([0, 30, 50, 80, 101]))))
+    min_area = int(g.choice([0, 4, 16, 64]))
+    inp = s.vbr_input("rect")
+    arrays = to_dev(inp)
+    A = sable.VbrMatrix(arrays, s.nrows, s.ncols, delta=s.delta,
+                        policy=dict(min_area=min_area, rules=rules))
+    try:
+        got = A.export()
+        want = oracle.partition(s.nrows, s.ncols, s.I, s.J, s.V.astype(np.float64), s.rpntr,
+                                s.cpntr, s.delta, min_area=min_area, rules=rules)
+        assert_partition_equal(got, want, dt, f"policy{seed}")
+        y = A.spmv(torch.from_numpy(s.x).cuda()).cpu().numpy()
+        yo, so = oracle.spmv(s.nrows, s.I, s.J, s.V.astype(np.float64), s.x.astype(np.float64))
+        assert_y_close(y, yo, so, dt, f"policy{seed}")
+    finally:
+        A.close()
+
+
+def test_delta_policy_rejected(sable):
+    s = gen.make("c1")
+    for pol in (dict(min_area=-1), dict(rules=[(1, 9, 1, 9, 102)]),
+                dict(rules=[(1, 2, 1, 2, 50)] * 65)):
+        with pytest.raises(sable.SableError) as e:
+            sable.VbrMatrix(to_dev(s.vbr_input("rect")), s.nrows, s.ncols, delta=50, policy=pol)
+        assert e.value.status == sable.SABLE_E_INVALID_ARG
