@@ -371,6 +371,21 @@ def make_c4(seed: int = 4, scale: float = 1.0) -> Synth:
                    meta=dict(keep_p=C4_KEEP_P))
 
 
+def make_c4a(seed: int = 4, scale: float = 1.0) -> Synth:
+    """The 64-aligned variant of configs[3] (SURVEY 8(d) C4 reading; the
+    delta-stress case of SURVEY 8(f) f2): the same matrix as C4, on the
+    64 x 64 tile grid instead of the union of the sub-blocks' edges, so every
+    candidate cell is a whole 64 x 64 tile holding one sub-block of 16..64 x
+    16..64 at fill 0.5..1 -- cell fills from 3% to 100%, where the delta rule
+    decides.  The GPU input is the all-remainder split."""
+    s = make_c4(seed, scale)
+    n = s.nrows
+    g = np.arange(0, n + 1, 64, dtype=np.int32)
+    s.name, s.rpntr, s.cpntr = "c4a", g, g.copy()
+    s.in_rect = np.zeros(s.nnz, dtype=bool)
+    return s
+
+
 C5_ALPHA = 2.5  # (inv.) power-law exponent of the remainder row degree
 
 
@@ -468,7 +483,8 @@ def make_c5(seed: int = 5, scale: float = 1.0) -> Synth:
                    meta=dict(dmin=dmin, alpha=C5_ALPHA))
 
 
-CONFIGS = {"c1": make_c1, "c2": make_c2, "c3": make_c3, "c4": make_c4, "c5": make_c5}
+CONFIGS = {"c1": make_c1, "c2": make_c2, "c3": make_c3, "c4": make_c4, "c5": make_c5,
+           "c4a": make_c4a}
 
 
 def make(name: str, scale: float = 1.0, seed: int | None = None) -> Synth:

@@ -186,9 +186,10 @@ __device__ __forceinline__ void dense_rows(const UPlan<T>& P, const Unit& U,
 }
 
 // Remainder part in waves of kRemWave entries (kRemKB coalesced loads per
-// lane): gathers x, stages the products and sums row `lane`'s entries in
-// [e0, e1) in entry order (valid for lane < nr), issuing wave w + 1's loads
-// before wave w's gather.
+// lane, the next wave's issued before this wave's gather): the products are
+// staged in shared memory and lane r sums row r's in entry order; a row with
+// more than 32 products in a wave is summed by the whole warp with a fixed
+// tree.
 constexpr int kRemKB = 4;
 constexpr int kRemWave = 32 * kRemKB;
 
@@ -211,45 +212,6 @@ __device__ __forceinline__ void rem_load(const UPlan<T>& P, int c0, int e1, int 
       w.c[k] = __ldcs(P.ridx + c0 + e);
       w.v[k] = __ldcs(P.rval + c0 + e);
     }
-  }
-}
-
-// A remainder of at most 32 entries (most units that also have dense rows):
-// one entry per lane (its column and value loaded before the dense part),
-// the products summed per row by a segmented inclusive scan over the lanes
-// (Hillis-Steele with row-head flags: a fixed tree per row), and row r's sum
-// taken from the lane of its last entry -- no shared memory, no barrier.
-template <typename T, int KV>
-__device__ __forceinline__ void rem_small(const Unit& U, const T* __restrict__ x, int lane,
-                                          int c, T v, int lo, int hi, T (&s)[KV]) {
-  const int n = U.e1 - U.e0;
-  T p[KV];
-  {
-    T xg[KV];
-#pragma unroll
-    for (int j = 0; j < KV; ++j) xg[j] = T(0);
-    if (lane < n) ldg_kv<T, KV>(x + (int64_t)c * KV, xg);
-#pragma unroll
-    for (int j = 0; j < KV; ++j) p[j] = v * xg[j];
-  }
-  const bool row = lane < U.nr && hi > lo;
-  const unsigned heads = __reduce_or_sync(kFull, row ? 1u << (lo - U.e0) : 0u) | 1u;
-  bool f = (heads >> lane) & 1u;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const bool ft = __shfl_up_sync(kFull, f, o);
-#pragma unroll
-    for (int j = 0; j < KV; ++j) {
-      const T t = __shfl_up_sync(kFull, p[j], o);
-      if (lane >= o && !f) p[j] += t;
-    }
-    if (lane >= o) f = f || ft;
-  }
-  const int src = row ? hi - 1 - U.e0 : 0;
-#pragma unroll
-  for (int j = 0; j < KV; ++j) {
-    const T t = __shfl_sync(kFull, p[j], src);
-    if (row) s[j] += t;
   }
 }
 
@@ -281,25 +243,10 @@ __device__ __forceinline__ void rem_rows(const UPlan<T>& P, const Unit& U,
     __syncwarp();
     const int a = max(lo, c0) - c0, b = min(hi, c0 + n) - c0;
     const bool longr = b - a > 32;
-    if (!longr) {
-      // four interleaved partial sums (entries e = a + 4i + m go to m), added
-      // in a fixed order: a short dependence chain, an order fixed by the row
+    if (!longr)
+      for (int e = a; e < b; ++e)
 #pragma unroll
-      for (int j = 0; j < KV; ++j) {
-        T q0 = T(0), q1 = T(0), q2 = T(0), q3 = T(0);
-        int e = a;
-        for (; e + 3 < b; e += 4) {
-          q0 += buf[e * KV + j];
-          q1 += buf[(e + 1) * KV + j];
-          q2 += buf[(e + 2) * KV + j];
-          q3 += buf[(e + 3) * KV + j];
-        }
-        if (e < b) q0 += buf[e * KV + j];
-        if (e + 1 < b) q1 += buf[(e + 1) * KV + j];
-        if (e + 2 < b) q2 += buf[(e + 2) * KV + j];
-        s[j] += (q0 + q1) + (q2 + q3);
-      }
-    }
+        for (int j = 0; j < KV; ++j) s[j] += buf[e * KV + j];
     unsigned lm = __ballot_sync(kFull, longr);
     while (lm) {
       const int q = __ffs(lm) - 1;
@@ -374,20 +321,12 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
     T s[KV];
 #pragma unroll
     for (int j = 0; j < KV; ++j) s[j] = T(0);
-    // remainder row bounds, and a short remainder's entries, in flight
-    // during the dense part
+    // the remainder's row bounds, in flight during the dense part
     const int ne = U.e1 - U.e0;
-    int lo = 0, hi = 0, rc = 0;
-    T rv = T(0);
-    if (ne > 0) {
-      if (lane < U.nr) {
-        lo = max(__ldg(P.rptr + U.row0 + lane), U.e0);
-        hi = min(__ldg(P.rptr + U.row0 + lane + 1), U.e1);
-      }
-      if (ne <= 32 && lane < ne) {
-        rc = __ldcs(P.ridx + U.e0 + lane);
-        rv = __ldcs(P.rval + U.e0 + lane);
-      }
+    int lo = 0, hi = 0;
+    if (ne > 0 && lane < U.nr) {
+      lo = max(__ldg(P.rptr + U.row0 + lane), U.e0);
+      hi = min(__ldg(P.rptr + U.row0 + lane + 1), U.e1);
     }
     if (U.wq > 0) {
       switch (U.llpr) {
@@ -399,10 +338,7 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
         default: dense_rows<T, 32, KV>(P, U, x, lane, s); break;
       }
     }
-    if (ne > 0 && ne <= 32)
-      rem_small<T, KV>(U, x, lane, rc, rv, lo, hi, s);
-    else if (ne > 0)
-      rem_rows<T, KV>(P, U, x, buf_s[warp], lane, lo, hi, s);
+    if (ne > 0) rem_rows<T, KV>(P, U, x, buf_s[warp], lane, lo, hi, s);
     finish_unit<T, KV>(P, U, s, y, lane);
   }
 }

@@ -3,7 +3,7 @@
 # launch list and one full ncu capture of the SpMV kernel per config.
 # usage: scripts/gpu_profile.sh TAG "c2 c4" [tests]
 set -u
-TAG=${1:-r01}
+TAG=${1:-r02}
 CFGS=${2:-"c2"}
 TESTS=${3:-tests}
 NCU=${4:-ncu}
@@ -21,8 +21,8 @@ for c in $CFGS; do
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
       --log-file $OUT/launches_$c.csv python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline \
       > $OUT/ncu_launch_$c.log 2>&1; echo "ncu launches $c rc=$?"
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:"spmv|rem_kernel" -s 6 -c 2 \
-      -o $OUT/spmv_$c python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline \
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:unit_kernel -s 3 -c 1 \
+      -o $OUT/unit_$c python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline \
       > $OUT/ncu_full_$c.log 2>&1; echo "ncu full $c rc=$?"
   fi
 done

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Summarise ncu captures for profiles/ (run here, no GPU needed).
 
-usage: python scripts/ncu_summary.py <dir with spmv_<cfg>.ncu-rep / launches_<cfg>.csv> <out.md>
+usage: python scripts/ncu_summary.py <dir with unit_<cfg>.ncu-rep / launches_<cfg>.csv> <out.md>
 
 For every config found: the top metrics of the --set full capture of the
 SpMV kernel (duration, DRAM bytes -> traffic per launch, DRAM / L2 / SM
@@ -70,8 +70,8 @@ def main():
     d, out = sys.argv[1], sys.argv[2]
     lines = [f"# ncu summary: {d}", ""]
     traffic = {}
-    for rep in sorted(glob.glob(os.path.join(d, "spmv_*.ncu-rep"))):
-        cfg = re.sub(r"^spmv_|\.ncu-rep$", "", os.path.basename(rep))
+    for rep in sorted(glob.glob(os.path.join(d, "unit_*.ncu-rep"))):
+        cfg = re.sub(r"^unit_|\.ncu-rep$", "", os.path.basename(rep))
         lines.append(f"## {cfg}: `ncu --set full` of the SpMV kernel")
         for i, k in enumerate(raw(rep)):
             name = k.get("Kernel Name", ("?", ""))[0]
@@ -96,16 +96,16 @@ def main():
     for lf in sorted(glob.glob(os.path.join(d, "launches_*.csv"))):
         cfg = re.sub(r"^launches_|\.csv$", "", os.path.basename(lf))
         rows = launch_shares(lf)
-        sp = [t for n, t in rows if "spmv" in n]
-        rm = [t for n, t in rows if "rem_kernel" in n]
+        uk = [t for n, t in rows if "unit_kernel" in n]
         lines.append(f"## {cfg}: launch list ({len(rows)} launches)")
         med = lambda v: sorted(v)[len(v) // 2] if v else 0.0  # noqa: E731
-        if sp or rm:
-            # one SpMV step = rem_kernel + spmv_kernel (+ the L2 scrub, not ours)
-            a, b = med(rm), med(sp)
-            lines.append(f"- rem_kernel launches: {len(rm)}, median {a * 1e6:.2f} us; "
-                         f"spmv_kernel launches: {len(sp)}, median {b * 1e6:.2f} us; "
-                         f"dense share of one SpMV: {b / max(a + b, 1e-12):.2f}")
+        if uk:
+            # one SpMV step = one unit_kernel launch (+ the L2 scrub, not ours)
+            timed = [t for n, t in rows if "unit_kernel" in n or "elementwise" in n or
+                     "reduce" in n]
+            lines.append(f"- unit_kernel launches: {len(uk)}, median {med(uk) * 1e6:.2f} us; "
+                         f"share of the device time of a timed step (SpMV + L2 scrub): "
+                         f"{sum(uk) / max(sum(timed), 1e-12):.2f}")
         tot = {}
         for n, t in rows:
             short = n.split("(")[0]

@@ -84,3 +84,24 @@ def test_both_arms_match_oracle(delta):
         A.close()
         yo, so = oracle.spmv(s.nrows, s.I, s.J, s.V.astype(np.float64), s.x.astype(np.float64))
         assert_y_close(y, yo, so, np.float32, f"{s.name}/d{delta}")
+
+
+def test_policy_from_heatmap():
+    b = calibrate.size_buckets([4, 16, 64])
+    assert b == {4: (1, 8), 16: (9, 32), 64: (33, 2 ** 31 - 1)}
+    heat = [dict(h=4, w=4, delta_star=None), dict(h=16, w=64, delta_star=70),
+            dict(h=64, w=16, delta_star=40)]
+    pol = calibrate.policy_from_heatmap(heat)
+    assert pol["delta"] == 50 and pol["min_area"] == 0
+    assert pol["rules"][0] == (1, 8, 1, 8, 101)
+    assert pol["rules"][1] == (9, 32, 33, 2 ** 31 - 1, 70)
+    assert pol["rules"][2] == (33, 2 ** 31 - 1, 9, 32, 40)
+
+
+def test_c4a_structure():
+    import gen
+    s = gen.make("c4a", scale=1 / 32)
+    assert np.all(np.diff(s.rpntr) == 64) and np.array_equal(s.rpntr, s.cpntr)
+    assert not s.in_rect.any()
+    c4 = gen.make("c4", scale=1 / 32)
+    assert s.nnz == c4.nnz  # the same matrix on another grid
