@@ -314,12 +314,17 @@ sable_status sable_partition_grid(int64_t nrows, int64_t ncols, int64_t nnz,
  *   X: device, row-major ncols x k (the k values of matrix column c at
  *      X[c*k .. c*k+k)), dtype of the handle; Y: device, row-major
  *      (row_end - row_begin) x k, fully written; not aliased with X.
- *   k in {1, 2, 4, 8} (else SABLE_E_UNSUPPORTED).  Asynchronous on
- *   cuda_stream; the first call allocates k-wide scratch (synchronously).
- * The same unit plan and kernel as sable_spmv with k accumulators per row
- * (one launch).  Each row's sums run in a fixed order (deterministic run to
- * run), within the SpMV tolerance of the definition; k = 1 is bitwise
- * sable_spmv, k > 1 folds lanes in a different fixed tree. */
+ *   k in {1, 2, 4, 8}: the SpMV's plan and kernel with k accumulators per row
+ *      (CUDA cores; k = 1 is bitwise sable_spmv, k > 1 folds lanes in another
+ *      fixed tree).
+ *   k in {16, 32, 64, 128}, fp32 handles only: every unit's panel rows times
+ *      the gathered X rows on the tensor cores (tcgen05.mma kind::tf32 into
+ *      TMEM, 3xTF32 split for fp32 accuracy; csrc/mma.cu), the remainder on
+ *      the CUDA cores in entry order.
+ *   Other k, or k >= 16 on fp64: SABLE_E_UNSUPPORTED.  Asynchronous on
+ *   cuda_stream; the first call per path allocates k-wide scratch
+ *   (synchronously).  Each row's sums run in a fixed order (deterministic
+ *   run to run), within the SpMV tolerance of the definition. */
 sable_status sable_spmm(sable_handle* h, const void* X, void* Y, int32_t k, void* cuda_stream);
 
 /* ---- handle images ---------------------------------

@@ -31,6 +31,8 @@ sable_status create_impl(const sable_vbr_desc* d, const sable_delta_policy* pol,
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st);
 cudaError_t run_spmm(const sable_handle* h, const void* X, void* Y, int32_t k, void* scratch,
                      cudaStream_t st);
+cudaError_t run_spmm_mma(const sable_handle* h, const void* X, void* Y, int32_t k, void* scratch,
+                         cudaStream_t st);
 sable_status comm_destroy(sable_handle* h);
 int32_t exec_grid(const sable_handle* h);
 
@@ -50,7 +52,7 @@ void free_handle(sable_handle* h) {
   if (!h) return;
   void* dev[] = {h->rem_ptr,  h->rem_idx,   h->rem_val,    h->pv,          h->units,
                  h->ubatch,   h->xq,        h->xside,      h->uxg,         h->uscratch,
-                 h->ucounters, h->mm_scratch, h->cell_br,  h->cell_bc,     h->cell_cnt,
+                 h->ucounters, h->mm_scratch, h->mma_scratch, h->cell_br,  h->cell_bc,     h->cell_cnt,
                  h->cell_dense, h->tiles,   h->tile_canon_off, h->tile_br, h->br_pbase,
                  h->br_W,     h->x_dev,     h->y_dev};
   for (void* p : dev)
@@ -337,21 +339,27 @@ sable_status sable_export_partition(const sable_handle* h, const sable_partition
 sable_status sable_spmm(sable_handle* h, const void* X, void* Y, int32_t k, void* cuda_stream) {
   if (!h || !X || (!Y && h->row_end > h->row_begin))
     return fail(SABLE_E_INVALID_ARG, "sable_spmm: NULL argument");
-  if (k != 1 && k != 2 && k != 4 && k != 8)
-    return fail(SABLE_E_UNSUPPORTED, "sable_spmm: k must be 1, 2, 4 or 8");
+  const bool cuda_cores = k == 1 || k == 2 || k == 4 || k == 8;
+  const bool tensor = k == 16 || k == 32 || k == 64 || k == 128;
+  if (!cuda_cores && !tensor)
+    return fail(SABLE_E_UNSUPPORTED, "sable_spmm: k must be 1, 2, 4, 8, 16, 32, 64 or 128");
+  if (tensor && h->dtype != SABLE_F32)
+    return fail(SABLE_E_UNSUPPORTED, "sable_spmm: k >= 16 (tensor cores, 3xTF32) needs fp32");
   DeviceGuard g(h->device);
   if (g.err) return cuda_fail(g.err, "sable_spmm: cudaSetDevice");
   const size_t sv = h->dtype == SABLE_F64 ? 8 : 4;
-  // k-wide partials of split row ranges: allocated once, for k = 8
-  if (!h->mm_scratch) {
-    const cudaError_t e =
-        cudaMalloc(&h->mm_scratch, sv * 8 * (size_t)std::max<int64_t>(h->uscratch_slots, 1));
+  // k-wide partials of split row ranges: allocated once (8 or 128 per slot)
+  void** scr = tensor ? &h->mma_scratch : &h->mm_scratch;
+  if (!*scr) {
+    const cudaError_t e = cudaMalloc(scr, sv * (tensor ? 128 : 8) *
+                                              (size_t)std::max<int64_t>(h->uscratch_slots, 1));
     if (e) {
-      h->mm_scratch = nullptr;
+      *scr = nullptr;
       return cuda_fail(e, "sable_spmm scratch");
     }
   }
-  const cudaError_t e = run_spmm(h, X, Y, k, h->mm_scratch, static_cast<cudaStream_t>(cuda_stream));
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  const cudaError_t e = tensor ? run_spmm_mma(h, X, Y, k, *scr, st) : run_spmm(h, X, Y, k, *scr, st);
   return e ? cuda_fail(e, "sable_spmm launch") : SABLE_OK;
 }
 

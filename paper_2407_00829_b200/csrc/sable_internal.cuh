@@ -190,6 +190,7 @@ struct sable_handle {
   void* uscratch = nullptr;
   int32_t* ucounters = nullptr;
   void* mm_scratch = nullptr;        // sable_spmm: 8 partials per slot (first use)
+  void* mma_scratch = nullptr;       // sable_spmm on the tensor cores: 128 partials per slot
   std::vector<int64_t> slice_batch;  // kSlices + 1 batch boundaries (host)
   std::vector<int64_t> slice_row;    // kSlices + 1 local row boundaries (host)
 

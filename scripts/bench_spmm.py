@@ -2,6 +2,7 @@
 """Time sable_spmm (Y = A X, k right-hand sides) against k
 separate sable_spmv calls at a config's full size; L2 flushed before each
 timed call, CUDA events on the launching stream.  One JSON line per (config, k).
+k = 1..8 run on the CUDA cores, k = 16..128 (fp32) on the tensor cores.
 usage: python scripts/bench_spmm.py [c2 c4 ...]"""
 import json
 import os
@@ -45,7 +46,8 @@ for name in sys.argv[1:] or ["c2"]:
     A = sable.VbrMatrix(arrays, s.nrows, s.ncols, delta=s.delta)
     del arrays
     tdt = torch.float64 if s.dtype == np.float64 else torch.float32
-    for k in (1, 2, 4, 8):
+    ks = (1, 2, 4, 8, 16, 32, 64, 128) if tdt == torch.float32 else (1, 2, 4, 8)
+    for k in ks:
         X = torch.randn((s.ncols, k), dtype=tdt, device="cuda")
         Y = torch.empty((s.nrows, k), dtype=tdt, device="cuda")
         xcols = [X[:, j].contiguous() for j in range(k)]
@@ -55,12 +57,14 @@ for name in sys.argv[1:] or ["c2"]:
         def kspmv():
             for j in range(k):
                 A.spmv(xcols[j], ys[j])
-        t_k = timed(kspmv)
+        t_k = timed(kspmv, reps=5 if k > 8 else 20)
         flops = 2.0 * s.nnz * k
         print(json.dumps({"bench": "spmm", "config": name, "k": k, "spmm_ms": round(t_mm, 4),
                           "k_spmv_ms": round(t_k, 4), "spmm_gflops": round(flops / t_mm / 1e6, 1),
                           "k_spmv_gflops": round(flops / t_k / 1e6, 1),
                           "speedup": round(t_k / t_mm, 3),
+                          "path": "tensor cores (tcgen05 kind::tf32, 3xTF32)" if k >= 16 else
+                                  "CUDA cores (unit_kernel, k accumulators)",
                           "bytes_alg_once": A.info["bytes_alg"],
                           "alg_gbs_spmm": round((A.info["bytes_alg"] +
                                                  (k - 1) * (s.ncols + s.nrows) *

@@ -98,6 +98,39 @@ def test_k_one_is_spmv(sable):
         A.close()
 
 
+@pytest.mark.parametrize("k", [16, 32, 64, 128])
+def test_tensor_core_k(sable, k):
+    """k >= 16 on the tensor cores (tcgen05.mma kind::tf32, 3xTF32): every
+    column within the SpMV tolerance of the oracle, deterministic."""
+    check(sable, gen.make("c1"), k)
+    check(sable, gen.random_small(70, 300, 280, 23, 19, density=0.3, dense_cells=0.5), k,
+          split="all_vbr")
+
+
+@pytest.mark.parametrize("name,scale", [("c2", 0.02), ("c4", 0.01), ("c5", 1 / 512)])
+def test_tensor_core_configs(sable, name, scale):
+    check(sable, gen.make(name, scale=scale), 32)
+
+
+def test_tensor_core_long_rows_and_wide_panels(sable, monkeypatch):
+    from test_gpu_parity import long_rows_synth
+    check(sable, long_rows_synth(), 64)  # remainder pieces meet in the combine scratch
+    monkeypatch.setenv("SABLE_USTAGE", "1024")  # panels cut into column chunks
+    check(sable, gen.random_small(71, 64, 3000, 2, 3, density=0.2, dense_cells=0.7), 16)
+
+
+def test_tensor_core_needs_fp32(sable):
+    s = gen.random_small(72, 100, 90, 7, 6, dtype=np.float64)
+    A = make(sable, s)
+    try:
+        X = torch.zeros((s.ncols, 16), dtype=torch.float64, device="cuda")
+        with pytest.raises(sable.SableError) as e:
+            A.spmm(X)
+        assert e.value.status == sable.SABLE_E_UNSUPPORTED
+    finally:
+        A.close()
+
+
 def test_bad_k(sable):
     s = gen.make("c1")
     A = make(sable, s)
