@@ -46,16 +46,18 @@ struct MmaSmem {
   int32_t last;
 };
 
-// Canonical no-swizzle layouts (16-byte units, core matrices of 8 x 16 B):
-// A (MN-major): element (m, kk) at (kk/8)*4096 + (m/4)*128 + (kk%8)*16 + (m%4)*4 bytes
-//   -> per K-group of 8: SBO = 128 B between m-chunks, LBO = 4096 B between K-groups.
-// B (K-major): element (n, kk) at ((kk/4)*(kN/8) + n/8)*128 + (n%8)*16 + (kk%4)*4 bytes
-//   -> SBO = 128 B between 8-row groups, LBO = 512 B between the two 16-byte K chunks.
-__device__ __forceinline__ int a_index(int m, int kk) {
-  return ((kk >> 3) * 4096 + (m >> 2) * 128 + (kk & 7) * 16 + (m & 3) * 4) >> 2;
-}
-__device__ __forceinline__ int b_index(int n, int kk) {
-  return (((kk >> 2) * (kN / 8) + (n >> 3)) * 128 + (n & 7) * 16 + (kk & 3) * 4) >> 2;
+// Canonical no-swizzle K-major layouts (core matrices of 8 rows x 16 B, i.e.
+// 4 tf32 along K): element (r, kk) of an R-row operand at
+//   (kk/4) * (R/8) * 128 + (r/8) * 128 + (r%8) * 16 + (kk%4) * 4 bytes
+// -> SBO = 128 B between 8-row groups, LBO = R/8 * 128 B between 16-byte K
+// chunks; one MMA (K = 8) spans two chunks.  Both operands are K-major: the
+// MN-major A of kind::tf32 measured all-zero accumulators on sm_100a
+// (scripts/probe/umma_probe.cu).
+constexpr int kLboA = kM / 8 * 128;  // 2048 B
+constexpr int kLboB = kN / 8 * 128;  // 512 B
+// 16-byte vector (4 consecutive kk) of row r in K chunk c, in floats
+__device__ __forceinline__ int kmaj_index(int lbo, int r, int c) {
+  return (c * lbo + (r >> 3) * 128 + (r & 7) * 16) >> 2;
 }
 
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -67,9 +69,9 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-// kind::tf32 instruction descriptor: F32 accumulator, TF32 A and B, A MN-major,
-// B K-major, N = kN, M = kM.
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (0u << 16) |
+// kind::tf32 instruction descriptor: F32 accumulator, TF32 A and B, both
+// K-major, N = kN, M = kM.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (0u << 16) |
                             ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
@@ -140,28 +142,41 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       const float* pv = P.pv + (int64_t)U.voff16 * 4;
       const int64_t rstride = (int64_t)U.wq * 4;
       for (int f0 = 0; f0 < W; f0 += kKT) {
-        // A tile: X rows of the panel columns f0 .. f0 + 31 (k values each,
-        // float4 per thread), split into tf32 hi / lo; zero past W and k
-        for (int i = tid; i < kKT * (kM / 4); i += kMmaThreads) {
-          const int kk = i / (kM / 4), mc = i % (kM / 4);
-          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (f0 + kk < W && mc * 4 < k)
-            v = __ldg(reinterpret_cast<const float4*>(X + (int64_t)panel_col(P, U.xq0, f0 + kk) * k) + mc);
-          const float e[4] = {v.x, v.y, v.z, v.w};
+        // A tile: thread m takes right-hand side m of the X rows under panel
+        // columns f0 + 4c .. f0 + 4c + 3 (each load coalesced over m), split
+        // into tf32 hi / lo, one 16-byte store each; zero past W and k
+#pragma unroll 2
+        for (int c = 0; c < kKT / 4; ++c) {
+          float e[4] = {0.f, 0.f, 0.f, 0.f};
+          if (f0 + 4 * c < W && m < k) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float hi = tf32_rna(e[q]);
-            S.a_hi[a_index(mc * 4 + q, kk)] = hi;
-            S.a_lo[a_index(mc * 4 + q, kk)] = tf32_rna(e[q] - hi);
+            for (int t = 0; t < 4; ++t)
+              e[t] = __ldg(X + (int64_t)panel_col(P, U.xq0, f0 + 4 * c + t) * k + m);
           }
+          float4 hi, lo;
+          hi.x = tf32_rna(e[0]); lo.x = tf32_rna(e[0] - hi.x);
+          hi.y = tf32_rna(e[1]); lo.y = tf32_rna(e[1] - hi.y);
+          hi.z = tf32_rna(e[2]); lo.z = tf32_rna(e[2] - hi.z);
+          hi.w = tf32_rna(e[3]); lo.w = tf32_rna(e[3] - hi.w);
+          const int o = kmaj_index(kLboA, m, c);
+          *reinterpret_cast<float4*>(S.a_hi + o) = hi;
+          *reinterpret_cast<float4*>(S.a_lo + o) = lo;
         }
-        // B tile: the unit's panel rows, columns f0 .. f0 + 31; zero past nr and W
-        for (int i = tid; i < kN * kKT; i += kMmaThreads) {
-          const int n = i / kKT, kk = i % kKT;
-          const float v = (n < nr && f0 + kk < W) ? __ldg(pv + n * rstride + f0 + kk) : 0.f;
-          const float hi = tf32_rna(v);
-          S.b_hi[b_index(n, kk)] = hi;
-          S.b_lo[b_index(n, kk)] = tf32_rna(v - hi);
+        // B tile: the unit's panel rows, columns f0 .. f0 + 31 as 16-byte
+        // vectors (rows are 16-byte padded); zero past nr and W
+        for (int i = tid; i < kN * (kKT / 4); i += kMmaThreads) {
+          const int n = i % kN, c = i / kN;
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (n < nr && f0 + 4 * c < W)
+            v = __ldg(reinterpret_cast<const float4*>(pv + n * rstride + f0 + 4 * c));
+          float4 hi, lo;
+          hi.x = tf32_rna(v.x); lo.x = tf32_rna(v.x - hi.x);
+          hi.y = tf32_rna(v.y); lo.y = tf32_rna(v.y - hi.y);
+          hi.z = tf32_rna(v.z); lo.z = tf32_rna(v.z - hi.z);
+          hi.w = tf32_rna(v.w); lo.w = tf32_rna(v.w - hi.w);
+          const int o = kmaj_index(kLboB, n, c);
+          *reinterpret_cast<float4*>(S.b_hi + o) = hi;
+          *reinterpret_cast<float4*>(S.b_lo + o) = lo;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
@@ -171,17 +186,18 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
           const uint32_t bh = smem_u32(S.b_hi), bl = smem_u32(S.b_lo);
 #pragma unroll
           for (int j = 0; j < kKT / 8; ++j) {
-            const uint64_t dah = smem_desc(ah + j * 4096, 4096, 128);
-            const uint64_t dal = smem_desc(al + j * 4096, 4096, 128);
-            const uint64_t dbh = smem_desc(bh + j * 2 * 512, 512, 128);
-            const uint64_t dbl = smem_desc(bl + j * 2 * 512, 512, 128);
+            const uint64_t dah = smem_desc(ah + j * 2 * kLboA, kLboA, 128);
+            const uint64_t dal = smem_desc(al + j * 2 * kLboA, kLboA, 128);
+            const uint64_t dbh = smem_desc(bh + j * 2 * kLboB, kLboB, 128);
+            const uint64_t dbl = smem_desc(bl + j * 2 * kLboB, kLboB, 128);
             mma_tf32(tmem, dah, dbh, (f0 > 0 || j > 0) ? 1u : 0u);
             mma_tf32(tmem, dah, dbl, 1u);
             mma_tf32(tmem, dal, dbh, 1u);
           }
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"(
-                           (uint64_t)__cvta_generic_to_shared(&S.bar))
-                       : "memory");
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                  bar)
+              : "memory");
         }
         mbar_wait(bar, phase);  // the tile's MMAs are done: its shared memory is free
         phase ^= 1u;
