@@ -35,8 +35,9 @@
 //               units (very long remainder rows, very wide panels) meet in
 //               scratch and the last piece to arrive sums the pieces in piece
 //               order.
-// While a unit computes, lane 0 pulls the next unit's data into L2 with bulk
-// prefetches (cp.async.bulk.prefetch.L2).  Every row's summation order is
+// At the start of a warp batch (4 consecutive units) lane 0 pulls the data of
+// the batch's later units into L2 with bulk prefetches
+// (cp.async.bulk.prefetch.L2).  Every row's summation order is
 // fixed by the matrix alone (the plan depends on the block row, never on the
 // shard count or on timing), so y is bitwise reproducible and identical for
 // every P.

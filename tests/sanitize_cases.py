@@ -1,7 +1,8 @@
 """Small cases for compute-sanitizer runs (tests/test_gpu_sanitize.py): C1,
 random grids in fp32/fp64, long remainder rows split into pieces, tiny unit
-budgets (column chunks, many combine groups), SpMM k = 4 and an iterated
-exchange step.  Exits 0 when every result matches the oracle."""
+budgets (column chunks, many combine groups), SpMM k = 4, tensor-core SpMM
+k = 16 and 128 (fp32) and an iterated exchange step.  Exits 0 when every
+result matches the oracle."""
 import os
 import sys
 
@@ -34,6 +35,11 @@ def run(s, split="rect"):
     X = torch.stack([x, 2 * x, -x, x], dim=1).contiguous()
     Y = A.spmm(X).cpu().numpy()
     assert_y_close(Y[:, 1] / 2, yo, so, s.dtype, s.name + " spmm")
+    if s.dtype == np.float32:  # the tensor-core path (k = 16 and 128)
+        for kk in (16, 128):
+            Xk = torch.stack([x * (1 + (j % 3)) for j in range(kk)], dim=1).contiguous()
+            Yk = A.spmm(Xk).cpu().numpy()
+            assert_y_close(Yk[:, kk - 2] / (1 + (kk - 2) % 3), yo, so, s.dtype, s.name + f" mma{kk}")
     if s.nrows == s.ncols:
         xn = torch.empty_like(x)
         A.spmv_allgather(x, xn)
