@@ -332,7 +332,7 @@ sable_status sable_spmm(sable_handle* h, const void* X, void* Y, int32_t k, void
  * -- the executor's unit plan (units, batches, x maps, combine groups), the
  * row-major panels, the remainder CSR, tile geometry, local cells, scalars
  * incl. the suitability flag of sable_get_info -- as one byte
- * image ("SABLEVC2": header with an FNV-1a
+ * image ("SABLEVC3": header with an FNV-1a
  * checksum, then fixed sections 8-byte aligned).  No NCCL state: call
  * sable_comm_init again on a world > 1 handle.  The image is tied to
  * SABLE_ABI_VERSION and to the executor configuration it was planned with.

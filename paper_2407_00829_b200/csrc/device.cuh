@@ -68,10 +68,67 @@ __device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
                  : "memory");
 }
 
-// A unit descriptor (32 B, read by every lane: one broadcast request).
-__device__ __forceinline__ Unit load_unit(const Unit* p) {
-  const int4* q = reinterpret_cast<const int4*>(p);
-  const int4 a = __ldg(q), b = __ldg(q + 1);
+// ---- shared memory, mbarriers and bulk copies (TMA engine, non-tensor)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Arrive once and expect `bytes` of bulk-copy transactions on the barrier.
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// Order this thread's (and, after __syncwarp, its warp's) generic-proxy
+// shared-memory accesses before later async-proxy (bulk copy) writes.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// Bulk copy global -> shared (cp.async.bulk, SASS UBLKCP), completion as
+// transaction bytes on `bar`; src, dst 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes,
+                                              uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ Unit unpack_unit(const int4& a, const int4& b) {
   Unit u;
   u.voff16 = a.x;
   u.row0 = a.y;
@@ -84,6 +141,23 @@ __device__ __forceinline__ Unit load_unit(const Unit* p) {
   u.llpr = (uint8_t)((b.w >> 8) & 0xff);
   u.piece = (uint16_t)((uint32_t)b.w >> 16);
   return u;
+}
+
+// A unit descriptor (32 B, read by every lane: one broadcast request).
+__device__ __forceinline__ Unit load_unit(const Unit* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  return unpack_unit(__ldg(q), __ldg(q + 1));
+}
+
+// A unit descriptor staged in shared memory.
+__device__ __forceinline__ Unit load_unit_smem(const void* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  return unpack_unit(q[0], q[1]);
+}
+
+__device__ __forceinline__ XMap ldg_xmap(const XMap* p) {
+  const int2 v = __ldg(reinterpret_cast<const int2*>(p));
+  return XMap{v.x, v.y};
 }
 
 // KV consecutive values of x (row-major ncols x KV) as one load where the

@@ -88,26 +88,16 @@ __device__ __forceinline__ float tf32_rna(float v) {
   return __uint_as_float(r);
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
 // Global column of panel column f of a unit (x map entry of its 4-column vector).
 __device__ __forceinline__ int panel_col(const UPlan<float>& P, int xq0, int f) {
-  const int m = __ldg(P.xq + xq0 + (f >> 2));
-  if (m >= 0) return min(m + (f & 3), P.nm1);
-  const int* side = reinterpret_cast<const int*>(P.xside + ~m);
-  return __ldg(side + (f & 3));
+  const XMap m = ldg_xmap(P.xq + xq0 + (f >> 2));
+  const int i = f & 3;
+  if (m.c >= 0) {
+    const int k = m.kd & 3, d = m.kd >> 2;
+    return min(m.c + i + (k != 0 && i >= k ? d : 0), P.nm1);
+  }
+  const int* side = reinterpret_cast<const int*>(P.xside + ~m.c);
+  return __ldg(side + i);
 }
 
 __global__ void __launch_bounds__(kMmaThreads, 1)
@@ -124,8 +114,8 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(1) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_init(bar, 1);
+    fence_mbar_init();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -178,7 +168,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
           *reinterpret_cast<float4*>(S.b_hi + o) = hi;
           *reinterpret_cast<float4*>(S.b_lo + o) = lo;
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        fence_proxy_async_smem();
         __syncthreads();
         if (tid == 0) {
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");

@@ -46,6 +46,8 @@ constexpr int64_t cover(int64_t bytes) { return bytes > 0 ? bytes + 32 : 0; }
 
 }  // namespace
 
+cudaError_t stage_setup(sable_handle* h, const Unit* hu, const int32_t* hbatch);  // unit.cu
+
 // Plan budgets (from the executor configuration, inspect.cu exec_config).
 struct UnitBudget {
   int64_t stage;        // cap on one unit's bytes (its data's aligned covers)
@@ -85,7 +87,7 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
     return std::max<int64_t>(1, (S - rp_bytes(nr) - 64) / ent);
   };
   std::vector<Unit> U;
-  std::vector<int32_t> xq;     // x map, one entry per column vector
+  std::vector<XMap> xq;        // x map, one entry per column vector
   std::vector<int32_t> xside;  // 4 columns per straddling column vector
   std::vector<XgU> xg;
   std::vector<PanelDesc> pd;
@@ -187,9 +189,17 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
         const int32_t c = col(f0, k);
         const int64_t run_end = k + 1 < R.size() ? R[k + 1].first : W;
         if (f0 + vec <= run_end || run_end == W) {
-          xq.push_back(c);
+          xq.push_back(XMap{c, 0});
+          continue;
+        }
+        // the first kA columns end run k, the rest lie in run k + 1 (d apart)
+        const int64_t kA = run_end - f0;
+        const int64_t end2 = k + 2 < R.size() ? R[k + 2].first : W;
+        const int64_t d = (int64_t)R[k + 1].second - ((int64_t)c + kA);
+        if ((f0 + vec <= end2 || end2 == W) && d >= -(1ll << 29) && d < (1ll << 29)) {
+          xq.push_back(XMap{c, (int32_t)(d * 4 + kA)});
         } else {
-          xq.push_back(~(int32_t)(xside.size() / 4));
+          xq.push_back(XMap{~(int32_t)(xside.size() / 4), 0});
           size_t k2 = k;
           int32_t last = c;
           for (int64_t i = 0; i < 4; ++i) {
@@ -202,7 +212,7 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
     pd.push_back(PanelDesc{br_vbase[la], pb, W, hgt});
     const int64_t vbase = pb / vec;  // panel base in 16-byte vectors
     const int64_t row_b = wq * 16;
-    const int64_t xm_b = cover(wq * 4);
+    const int64_t xm_b = cover(wq * (int64_t)sizeof(XMap));
     if (row_b + xm_b + rp_bytes(1) + 64 + ent <= S) {
       // row groups: as many rows as the lanes' accumulators and a stage hold
       const int llpr = choose_llpr(wq);
@@ -303,19 +313,19 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
   h->uscratch_slots = slot;
   auto up = [&](void** dst, const void* src, size_t bytes) {
     if (e) return;
-    e = cudaMalloc(dst, bytes ? bytes : 16);
+    e = cudaMalloc(dst, bytes + 16);  // +16 B: the staged executor's 16-byte covers
     if (!e && bytes) e = cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, st);
   };
   up(reinterpret_cast<void**>(&h->units), U.data(), sizeof(Unit) * U.size());
   up(reinterpret_cast<void**>(&h->ubatch), batch.data(), sizeof(int32_t) * batch.size());
-  up(reinterpret_cast<void**>(&h->xq), xq.data(), sizeof(int32_t) * xq.size());
+  up(reinterpret_cast<void**>(&h->xq), xq.data(), sizeof(XMap) * xq.size());
   up(reinterpret_cast<void**>(&h->xside), xside.data(), sizeof(int32_t) * xside.size());
   up(reinterpret_cast<void**>(&h->uxg), xg.data(), sizeof(XgU) * xg.size());
   if (!e) e = cudaMalloc(&h->uscratch, (size_t)std::max<int64_t>(slot, 1) * sv);
   if (!e) e = cudaMalloc(reinterpret_cast<void**>(&h->ucounters),
                          sizeof(int32_t) * std::max<size_t>(xg.size(), 1));
   if (!e) e = cudaMemsetAsync(h->ucounters, 0, sizeof(int32_t) * std::max<size_t>(xg.size(), 1), st);
-  if (!e) e = cudaMalloc(&h->pv, (size_t)std::max<int64_t>(pb, 1) * sv);
+  if (!e) e = cudaMalloc(&h->pv, (size_t)std::max<int64_t>(pb, 1) * sv + 16);
   PanelDesc* pd_d = nullptr;
   if (!e && !pd.empty()) {
     e = cudaMalloc(reinterpret_cast<void**>(&pd_d), sizeof(PanelDesc) * pd.size());
@@ -329,6 +339,7 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
   }
   if (pd_d) cudaFree(pd_d);
   if (!e) e = cudaStreamSynchronize(st);
+  if (!e) e = stage_setup(h, U.data(), batch.data());
   return e;
 }
 

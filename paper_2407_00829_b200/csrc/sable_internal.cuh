@@ -8,9 +8,9 @@
 //            pv[base_a + r * Wp].  For one tile this is the tile transposed
 //            from the paper's column-major storage (
 //            reading R8: the internal layout is free).
-//   xq     : per panel, one int32 per 16-byte column vector: the global
-//            column of its first column (xside for vectors straddling two
-//            runs of global columns).
+//   xq     : per panel, one XMap (8 B) per 16-byte column vector: the global
+//            columns of its N columns (xside for vectors spanning three or
+//            more runs of global columns).
 //   units  : the executor's work list (plan.cu), batches of consecutive
 //            units per warp.
 //   rem_*  : the CSR remainder of the local rows (int32 row pointers).
@@ -47,11 +47,13 @@ struct XTile {
 // Executor configuration (runtime; SABLE_* environment overrides are for
 // tuning and tests, validated by inspect.cu's exec_config).
 struct ExecCfg {
-  int32_t pf;          // 1: bulk L2 prefetch of the next unit's data (SABLE_XPREFETCH)
+  int32_t pf;          // L2 bulk prefetch bits (SABLE_XPREFETCH; inspect.cu exec_config)
   int32_t ustage;      // cap on one unit's bytes (SABLE_USTAGE; plan.cu)
   int32_t rem_rows;    // rows per remainder-only unit (SABLE_UREM_ROWS)
   int32_t batch;       // units per warp batch (SABLE_UBATCH_UNITS)
   int32_t sliced;      // 1: world-1 exchange steps run the slice launches (SABLE_SLICED, tests)
+  int32_t exec;        // SpMV executor: 0 unit_kernel (batches), 1 wunit_kernel (SABLE_EXEC=unit|window)
+  int32_t unit_cost;   // windowed executor: per-unit overhead in bytes for the warp ranges (SABLE_UNIT_COST)
 };
 
 // ---- the unit executor (unit.cu, plan.cu)
@@ -76,11 +78,19 @@ struct Unit {        // 32 B
 };
 static_assert(sizeof(Unit) == 32, "Unit is 32 B");
 
-// x map of a panel, one int32 per 16-byte column vector q (panel columns
-// vN .. vN + N - 1, N = 16 / sizeof(T)): c >= 0 -- the vector's columns read
-// x[c], x[c + 1], ... (clamped to ncols - 1: columns past the panel width
-// hold zero values); c < 0 -- the vector straddles a run boundary and its N
+// x map of a panel, one XMap per 16-byte column vector q (panel columns
+// qN .. qN + N - 1, N = 16 / sizeof(T)): c >= 0 -- column i of the vector
+// reads x[c + i] for i < k and x[c + i + d] for i >= k, where k = kd & 3 and
+// d = kd >> 2 (k = 0: the vector lies in one run of consecutive global
+// columns; k > 0: its first k columns end one run and the rest start the
+// next, d apart), clamped to ncols - 1 (columns past the panel width hold
+// zero values); c < 0 -- the vector spans three or more runs and its N
 // global columns are xside[~c] (int32 each, padded to 16 B).
+struct XMap {
+  int32_t c;
+  int32_t kd;
+};
+static_assert(sizeof(XMap) == 8, "XMap is 8 B");
 
 struct XgU {         // combine group of split units (16 B)
   int64_t slot;      // scratch base (npieces * 32 partials)
@@ -93,7 +103,7 @@ static_assert(sizeof(XgU) == 16, "XgU is 16 B");
 #define SABLE_UNIT_WARPS 1  // A/B builds: warps per unit-executor CTA (1: measured r02)
 #endif
 constexpr int kUnitWarps = SABLE_UNIT_WARPS;
-constexpr int kUnitBytes = 32768;  // default cap on one unit's data (plan.cu)
+constexpr int kUnitBytes = 32768;  // default cap on one unit's data (plan.cu), unit_kernel
 constexpr int kUnitBatch = 4;      // default units per warp batch
 constexpr int kSlices = 8;         // exchange slices of a shard (comm.cu overlap)
 
@@ -101,7 +111,7 @@ template <typename T>
 struct UPlan {
   const Unit* units;
   const int32_t* batch;   // n_batches + 1 unit boundaries (one batch per warp)
-  const int32_t* xq;      // x maps of the panels
+  const XMap* xq;         // x maps of the panels
   const int4* xside;      // columns of straddling vectors
   const T* pv;
   const int32_t* rptr;    // local remainder row pointers
@@ -180,7 +190,7 @@ struct sable_handle {
   int64_t n_units = 0;
   int32_t* ubatch = nullptr;         // n_ubatch + 1
   int64_t n_ubatch = 0;
-  int32_t* xq = nullptr;
+  sable::XMap* xq = nullptr;
   int64_t n_xq = 0;
   int4* xside = nullptr;
   int64_t n_xside = 0;
@@ -193,6 +203,10 @@ struct sable_handle {
   void* mma_scratch = nullptr;       // sable_spmm on the tensor cores: 128 partials per slot
   std::vector<int64_t> slice_batch;  // kSlices + 1 batch boundaries (host)
   std::vector<int64_t> slice_row;    // kSlices + 1 local row boundaries (host)
+  // windowed executor (unit.cu stage_setup): persistent grid of st_G warps,
+  // per-warp unit ranges for the whole shard and for each exchange slice
+  int32_t* st_wcut = nullptr;        // (1 + kSlices) * (st_G + 1)
+  int64_t st_G = 0;                  // 0: the windowed executor is off
 
   // export data (device): local cells and tile geometry
   int32_t* cell_br = nullptr;

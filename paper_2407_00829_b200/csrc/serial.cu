@@ -24,10 +24,11 @@
 namespace sable {
 
 void free_handle(sable_handle* h);
+cudaError_t stage_setup(sable_handle* h, const Unit* hu, const int32_t* hbatch);  // unit.cu
 
 namespace {
 
-constexpr char kMagic[8] = {'S', 'A', 'B', 'L', 'E', 'V', 'C', '2'};
+constexpr char kMagic[8] = {'S', 'A', 'B', 'L', 'E', 'V', 'C', '3'};
 constexpr int kSections = 22;
 
 struct ImageHeader {
@@ -64,7 +65,7 @@ std::vector<Section> sections(sable_handle* h) {
   return {
       {h->units, nullptr, (int64_t)sizeof(Unit) * h->n_units},
       {h->ubatch, nullptr, 4 * (h->n_ubatch + 1)},
-      {h->xq, nullptr, 4 * h->n_xq},
+      {h->xq, nullptr, (int64_t)sizeof(XMap) * h->n_xq},
       {h->xside, nullptr, 16 * h->n_xside},
       {h->uxg, nullptr, (int64_t)sizeof(XgU) * h->n_uxg},
       {h->pv, nullptr, sv * h->pv_elems},
@@ -207,11 +208,17 @@ std::string check_image(const ImageHeader& H, const unsigned char* in,
   for (int64_t e = 0; e < H.rem_nnz; ++e)
     if (ridx[e] < 0 || ridx[e] >= H.ncols) return "rem_indices";
   // x maps
-  const int32_t* xq = sec<int32_t>(in, off, 2);
+  const XMap* xq = sec<XMap>(in, off, 2);
   const int32_t* xside = sec<int32_t>(in, off, 3);
-  for (int64_t i = 0; i < H.n_xq; ++i)
-    if ((xq[i] >= 0 && xq[i] >= H.ncols) || (xq[i] < 0 && (int64_t)~xq[i] >= H.n_xside))
-      return "x map";
+  for (int64_t i = 0; i < H.n_xq; ++i) {
+    const XMap m = xq[i];
+    if (m.c < 0) {
+      if ((int64_t)~m.c >= H.n_xside) return "x map";
+      continue;
+    }
+    const int64_t k = m.kd & 3, d = m.kd >> 2;  // second run starts at column c + k + d
+    if (m.c >= H.ncols || (k != 0 && (m.c + k + d < 0 || m.c + k + d >= H.ncols))) return "x map";
+  }
   for (int64_t i = 0; i < 4 * H.n_xside; ++i)
     if (xside[i] < 0 || xside[i] >= H.ncols) return "x side map";
   // combine groups
@@ -320,7 +327,7 @@ extern "C" sable_status sable_deserialize(const void* buf, int64_t size, void* c
   const unsigned char* in = static_cast<const unsigned char*>(buf);
   ImageHeader H;
   memcpy(&H, in, sizeof(H));
-  if (memcmp(H.magic, kMagic, 8) != 0) return fail(SABLE_E_FORMAT, "sable_deserialize: not a SABLEVC2 image");
+  if (memcmp(H.magic, kMagic, 8) != 0) return fail(SABLE_E_FORMAT, "sable_deserialize: not a SABLEVC3 image");
   if (H.abi_version != SABLE_ABI_VERSION || H.header_bytes != (int32_t)sizeof(ImageHeader) ||
       H.sizeof_unit != (int32_t)sizeof(Unit) || H.sizeof_xgu != (int32_t)sizeof(XgU) ||
       H.sizeof_tiledesc != (int32_t)sizeof(TileDesc) || H.sizeof_cfg != (int32_t)sizeof(ExecCfg) ||
@@ -331,8 +338,9 @@ extern "C" sable_status sable_deserialize(const void* buf, int64_t size, void* c
       H.br_end > H.nbr || H.row_begin < 0 || H.row_end < H.row_begin || H.row_end > H.nrows ||
       H.nrows < 1 || H.ncols < 1 || H.nrows >= (1ll << 31) - 1 || H.ncols >= (1ll << 31) - 1)
     return fail(SABLE_E_FORMAT, "sable_deserialize: inconsistent header");
-  if (H.cfg.pf < 0 || H.cfg.pf > 1 || H.cfg.ustage < 1024 || H.cfg.ustage % 16 != 0 ||
-      H.cfg.ustage > (1 << 24) || H.cfg.rem_rows < 1 || H.cfg.rem_rows > 32 || H.cfg.batch < 1)
+  if (H.cfg.pf < 0 || H.cfg.pf > 3 || H.cfg.ustage < 1024 || H.cfg.ustage % 16 != 0 ||
+      H.cfg.ustage > (1 << 24) || H.cfg.rem_rows < 1 || H.cfg.rem_rows > 32 || H.cfg.batch < 1 ||
+      H.cfg.exec < 0 || H.cfg.exec > 1 || H.cfg.unit_cost < 0 || H.cfg.unit_cost > (1 << 24))
     return fail(SABLE_E_FORMAT, "sable_deserialize: executor configuration out of range");
   {
     const int64_t lim = (int64_t)1 << 40;  // bounds every count so that byte sizes cannot wrap
@@ -418,6 +426,10 @@ extern "C" sable_status sable_deserialize(const void* buf, int64_t size, void* c
   dal((void**)&h->ucounters, 4 * h->n_uxg);
   if (!e) e = cudaMemsetAsync(h->ucounters, 0, 4 * (size_t)std::max<int64_t>(h->n_uxg, 1), st);
   if (!e) e = cudaStreamSynchronize(st);  // the host image may be released on return
+  // the persistent executors' per-warp unit ranges (device dependent: recomputed here)
+  if (!e)
+    e = stage_setup(h, reinterpret_cast<const Unit*>(in + offs[0]),
+                    reinterpret_cast<const int32_t*>(in + offs[1]));
   if (e) {
     set_error(cuda_msg(e, "sable_deserialize"));
     cudaStreamSynchronize(st);
