@@ -20,6 +20,7 @@ struct Vec<float> {
     return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
   }
   static __device__ __forceinline__ float4 zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  static __device__ __forceinline__ float4 one() { return make_float4(1.f, 1.f, 1.f, 1.f); }
 };
 template <>
 struct Vec<double> {
@@ -29,6 +30,7 @@ struct Vec<double> {
     return i == 0 ? v.x : v.y;
   }
   static __device__ __forceinline__ double2 zero() { return make_double2(0.0, 0.0); }
+  static __device__ __forceinline__ double2 one() { return make_double2(1.0, 1.0); }
 };
 
 // Arrival counter of a split row range: releases this warp's scratch writes

@@ -94,7 +94,7 @@ __device__ __forceinline__ int panel_col(const UPlan<float>& P, int xq0, int f) 
   const int i = f & 3;
   if (m.c >= 0) {
     const int k = m.kd & 3, d = m.kd >> 2;
-    return min(m.c + i + (k != 0 && i >= k ? d : 0), P.nm1);
+    return m.c + i + (i >= k ? d : 0);
   }
   const int* side = reinterpret_cast<const int*>(P.xside + ~m.c);
   return __ldg(side + i);
@@ -280,7 +280,6 @@ cudaError_t run_spmm_mma(const sable_handle* h, const void* X, void* Y, int32_t 
   P.counters = h->ucounters;
   P.b0 = 0;
   P.n_batches = h->n_ubatch;
-  P.nm1 = (int32_t)(h->ncols - 1);
   P.pf = 0;
   int dev = 0, sms = 148;
   cudaError_t e = cudaGetDevice(&dev);

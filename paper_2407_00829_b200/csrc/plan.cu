@@ -184,28 +184,49 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
         while (kk + 1 < R.size() && R[kk + 1].first <= f) ++kk;
         return (int32_t)(R[kk].second + (f - R[kk].first));
       };
+      // every column index an entry yields is in [0, ncols) (no clamp on the
+      // device): padding columns past W (zero values) continue the last run
+      // when that stays inside the matrix, else read columns 0, 1, ...
+      const int64_t ncols = h->ncols;
+      auto encode = [&](const int64_t* cc) -> bool {
+        for (int64_t i = 0; i < vec; ++i)
+          if (cc[i] < 0 || cc[i] >= ncols) return false;
+        for (int64_t kk = 0; kk < vec; ++kk) {  // kk = 0: one run; else split before kk
+          bool ok = true;
+          for (int64_t i = 0; i < vec && ok; ++i)
+            ok = i < kk || kk == 0 ? cc[i] == cc[0] + i : cc[i] == cc[kk] + (i - kk);
+          const int64_t d = kk == 0 ? 0 : cc[kk] - (cc[0] + kk);
+          if (ok && d >= -(1ll << 29) && d < (1ll << 29)) {
+            xq.push_back(XMap{(int32_t)cc[0], (int32_t)(d * 4 + kk)});
+            return true;
+          }
+        }
+        return false;
+      };
       for (int64_t q = 0; q < wq; ++q) {
         const int64_t f0 = q * vec;
-        const int32_t c = col(f0, k);
-        const int64_t run_end = k + 1 < R.size() ? R[k + 1].first : W;
-        if (f0 + vec <= run_end || run_end == W) {
-          xq.push_back(XMap{c, 0});
-          continue;
-        }
-        // the first kA columns end run k, the rest lie in run k + 1 (d apart)
-        const int64_t kA = run_end - f0;
-        const int64_t end2 = k + 2 < R.size() ? R[k + 2].first : W;
-        const int64_t d = (int64_t)R[k + 1].second - ((int64_t)c + kA);
-        if ((f0 + vec <= end2 || end2 == W) && d >= -(1ll << 29) && d < (1ll << 29)) {
-          xq.push_back(XMap{c, (int32_t)(d * 4 + kA)});
-        } else {
-          xq.push_back(XMap{~(int32_t)(xside.size() / 4), 0});
-          size_t k2 = k;
-          int32_t last = c;
-          for (int64_t i = 0; i < 4; ++i) {
-            if (i < vec && f0 + i < W) last = col(f0 + i, k2);
-            xside.push_back(last);
+        int64_t cc[4], last = 0;
+        size_t k2 = k;
+        for (int64_t i = 0; i < vec; ++i) {
+          if (f0 + i < W) {
+            last = col(f0 + i, k2);
+            cc[i] = last;
+          } else {
+            cc[i] = last + (f0 + i - (W - 1));
           }
+        }
+        col(f0, k);  // advance the run cursor
+        if (encode(cc)) continue;
+        if (f0 + vec > W) {
+          for (int64_t i = 0; i < vec; ++i)
+            if (f0 + i >= W) cc[i] = f0 + i - W;
+          if (encode(cc)) continue;
+        }
+        // three or more runs (or no encodable padding): the side table
+        xq.push_back(XMap{~(int32_t)(xside.size() / 4), 0});
+        for (int64_t i = 0; i < 4; ++i) {
+          if (i < vec && f0 + i < W) last = cc[i];
+          xside.push_back((int32_t)last);
         }
       }
     }

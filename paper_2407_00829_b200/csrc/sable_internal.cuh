@@ -81,11 +81,13 @@ static_assert(sizeof(Unit) == 32, "Unit is 32 B");
 // x map of a panel, one XMap per 16-byte column vector q (panel columns
 // qN .. qN + N - 1, N = 16 / sizeof(T)): c >= 0 -- column i of the vector
 // reads x[c + i] for i < k and x[c + i + d] for i >= k, where k = kd & 3 and
-// d = kd >> 2 (k = 0: the vector lies in one run of consecutive global
-// columns; k > 0: its first k columns end one run and the rest start the
-// next, d apart), clamped to ncols - 1 (columns past the panel width hold
-// zero values); c < 0 -- the vector spans three or more runs and its N
-// global columns are xside[~c] (int32 each, padded to 16 B).
+// d = kd >> 2 (k = 0, d = 0: the vector lies in one run of consecutive
+// global columns; k > 0: its first k columns end one run and the rest start
+// the next, d apart); columns past the panel width hold zero values and read
+// any column inside the matrix; every column an entry yields is in
+// [0, ncols) (plan.cu), so the executors never clamp; c < 0 -- the vector
+// spans three or more runs and its N global columns are xside[~c] (int32
+// each, padded to 16 B).
 struct XMap {
   int32_t c;
   int32_t kd;
@@ -121,7 +123,6 @@ struct UPlan {
   T* scratch;
   int32_t* counters;
   int64_t b0, n_batches;  // batches [b0, n_batches) of this launch
-  int32_t nm1;            // ncols - 1
   int32_t pf;             // 1: bulk L2 prefetch of the next unit's data
 };
 

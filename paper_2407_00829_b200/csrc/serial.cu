@@ -216,8 +216,12 @@ std::string check_image(const ImageHeader& H, const unsigned char* in,
       if ((int64_t)~m.c >= H.n_xside) return "x map";
       continue;
     }
-    const int64_t k = m.kd & 3, d = m.kd >> 2;  // second run starts at column c + k + d
-    if (m.c >= H.ncols || (k != 0 && (m.c + k + d < 0 || m.c + k + d >= H.ncols))) return "x map";
+    const int64_t k = m.kd & 3, d = m.kd >> 2, vec = H.dtype == SABLE_F64 ? 2 : 4;
+    if (k >= vec || (k == 0 && d != 0)) return "x map";
+    for (int64_t i = 0; i < vec; ++i) {  // every column the executors read
+      const int64_t c = m.c + i + (i >= k ? d : 0);
+      if (c < 0 || c >= H.ncols) return "x map";
+    }
   }
   for (int64_t i = 0; i < 4 * H.n_xside; ++i)
     if (xside[i] < 0 || xside[i] >= H.ncols) return "x side map";

@@ -83,17 +83,16 @@ __device__ __forceinline__ void prefetch_span(const UPlan<T>& P, const Unit& A, 
 
 // x (row-major ncols x KV) of the N columns of one panel column vector,
 // x map entry m (sable_internal.cuh XMap: c >= 0 -- columns c + i, the ones
-// from i = k on shifted by d, clamped to ncols - 1; c < 0 -- the side entry
-// ~c lists the N columns).
+// from i = k on shifted by d, all inside [0, ncols) by construction; c < 0 --
+// the side entry ~c lists the N columns).
 template <typename T, int KV>
 __device__ __forceinline__ void load_xv(const UPlan<T>& P, XMap m, const T* __restrict__ x,
                                         T (&xv)[Vec<T>::N][KV]) {
   constexpr int N = Vec<T>::N;
   if (m.c >= 0) {
-    const int k = m.kd & 3, d = m.kd >> 2;
+    const int k = m.kd & 3, d = m.kd >> 2;  // k = 0: d = 0
 #pragma unroll
-    for (int i = 0; i < N; ++i)
-      ldg_kv<T, KV>(x + (int64_t)min(m.c + i + (k != 0 && i >= k ? d : 0), P.nm1) * KV, xv[i]);
+    for (int i = 0; i < N; ++i) ldg_kv<T, KV>(x + (int64_t)(m.c + i + (i >= k ? d : 0)) * KV, xv[i]);
   } else {
     const int4 c = __ldg(P.xside + ~m.c);
     ldg_kv<T, KV>(x + (int64_t)c.x * KV, xv[0]);
@@ -493,7 +492,6 @@ UPlan<T> make_plan(const sable_handle* h, void* scratch) {
   P.counters = h->ucounters;
   P.b0 = 0;
   P.n_batches = h->n_ubatch;
-  P.nm1 = (int32_t)(h->ncols - 1);
   P.pf = h->cfg.pf;
   return P;
 }
