@@ -1,6 +1,6 @@
 // abi.cu -- the extern "C" entry points of libsable.so (include/sable.h).
 // Argument checking, error text, handle lifetime, info and the canonical
-// partition export.  The arithmetic lives in inspect.cu and exec.cu.
+// partition export.  The arithmetic lives in inspect.cu, plan.cu and unit.cu.
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
@@ -54,7 +54,7 @@ void free_handle(sable_handle* h) {
                  h->ubatch,   h->xq,        h->xside,      h->uxg,         h->uscratch,
                  h->ucounters, h->mm_scratch, h->mma_scratch, h->cell_br,  h->cell_bc,     h->cell_cnt,
                  h->cell_dense, h->tiles,   h->tile_canon_off, h->tile_br, h->br_pbase,
-                 h->br_W,     h->x_dev,     h->y_dev,       h->st_wcut};
+                 h->br_W,     h->x_dev,     h->y_dev};
   for (void* p : dev)
     if (p) cudaFree(p);
   free(h->all_bounds_h);

@@ -536,31 +536,19 @@ int64_t env_int(const char* name, int64_t dflt) {
 // defaults (tuning runs and tests).  Invalid overrides -> SABLE_E_INVALID_ARG.
 ExecCfg exec_config() {
   ExecCfg c{};
-  c.pf = -1;
-  {
-    const char* ex = std::getenv("SABLE_EXEC");
-    const std::string es = ex ? ex : "window";
-    if (es != "unit" && es != "window") {
-      set_error("invalid SABLE_EXEC (unit | window)");
-      throw Fail{SABLE_E_INVALID_ARG};
-    }
-    c.exec = es == "window" ? 1 : 0;
-  }
-  c.unit_cost = (int32_t)env_int("SABLE_UNIT_COST", 2048);
-  // L2 bulk prefetch: bit 0 the data of the next units (unit_kernel: per
-  // batch), bit 1 (windowed executor) the x-map and row-pointer spans per window
-  c.pf = (int32_t)env_int("SABLE_XPREFETCH", c.exec == 1 ? 2 : 1);
+  c.pf = (int32_t)env_int("SABLE_XPREFETCH", 1);
   c.ustage = (int32_t)env_int("SABLE_USTAGE", kUnitBytes);
   c.rem_rows = (int32_t)env_int("SABLE_UREM_ROWS", 32);
   c.batch = (int32_t)env_int("SABLE_UBATCH_UNITS", kUnitBatch);
+  c.batch_bytes = (int32_t)env_int("SABLE_UBATCH_BYTES", kBatchBytes);
   c.sliced = env_int("SABLE_SLICED", 0) != 0 ? 1 : 0;
   const int64_t arch = env_int("SABLE_ARCH", 2);
   if (arch != 2 || c.ustage < 1024 || c.ustage % 16 != 0 || c.ustage > (1 << 24) ||
-      c.rem_rows < 1 || c.rem_rows > 32 || c.batch < 1 || c.pf < 0 || c.pf > 3 ||
-      c.unit_cost < 0 || c.unit_cost > (1 << 24)) {
+      c.rem_rows < 1 || c.rem_rows > 32 || c.batch < 1 || (c.pf != 0 && c.pf != 1) ||
+      c.batch_bytes < 1) {
     set_error("invalid SABLE_ARCH / SABLE_USTAGE / SABLE_UREM_ROWS / SABLE_UBATCH_UNITS / "
-              "SABLE_XPREFETCH (arch 2 only; ustage a multiple of 16 in [1024, 2^24]; "
-              "1..32 rows; batch >= 1)");
+              "SABLE_UBATCH_BYTES / SABLE_XPREFETCH (arch 2 only; ustage a multiple of 16 in "
+              "[1024, 2^24]; 1..32 rows; batch >= 1; batch bytes >= 1)");
     throw Fail{SABLE_E_INVALID_ARG};
   }
   return c;

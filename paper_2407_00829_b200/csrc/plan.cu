@@ -46,13 +46,12 @@ constexpr int64_t cover(int64_t bytes) { return bytes > 0 ? bytes + 32 : 0; }
 
 }  // namespace
 
-cudaError_t stage_setup(sable_handle* h, const Unit* hu, const int32_t* hbatch);  // unit.cu
-
 // Plan budgets (from the executor configuration, inspect.cu exec_config).
 struct UnitBudget {
   int64_t stage;        // cap on one unit's bytes (its data's aligned covers)
   int64_t rem_rows;     // rows per remainder-only unit (<= 32)
-  int64_t batch_units;  // units per warp batch
+  int64_t batch_units;  // max units per warp batch
+  int64_t batch_bytes;  // a batch closes once its units hold this many bytes
 };
 
 UnitBudget unit_budget(const ExecCfg& c) {
@@ -60,6 +59,7 @@ UnitBudget unit_budget(const ExecCfg& c) {
   b.stage = c.ustage;
   b.rem_rows = c.rem_rows;
   b.batch_units = c.batch;
+  b.batch_bytes = c.batch_bytes;
   return b;
 }
 
@@ -317,7 +317,15 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
   for (int s = 0; s < kSlices; ++s) {
     h->slice_batch[s] = (int64_t)batch.size();
     h->slice_row[s] = ucut[s] < (int64_t)U.size() ? U[ucut[s]].row0 : nloc;
-    for (int64_t i = ucut[s]; i < ucut[s + 1]; i += B.batch_units) batch.push_back((int32_t)i);
+    // a batch closes at batch_units units or batch_bytes bytes, whichever
+    // comes first, so batches are comparable in work and the CTA scheduler
+    // balances them dynamically
+    int64_t nb = 0, bb = 0;
+    for (int64_t i = ucut[s]; i < ucut[s + 1]; ++i) {
+      if (nb == 0) batch.push_back((int32_t)i);
+      bb += (int64_t)U[i].nr * U[i].wq * 16 + (int64_t)(U[i].e1 - U[i].e0) * ent + 64;
+      if (++nb >= B.batch_units || bb >= B.batch_bytes) nb = bb = 0;
+    }
   }
   h->slice_batch[kSlices] = (int64_t)batch.size();
   h->slice_row[kSlices] = nloc;
@@ -360,7 +368,6 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
   }
   if (pd_d) cudaFree(pd_d);
   if (!e) e = cudaStreamSynchronize(st);
-  if (!e) e = stage_setup(h, U.data(), batch.data());
   return e;
 }
 

@@ -47,13 +47,12 @@ struct XTile {
 // Executor configuration (runtime; SABLE_* environment overrides are for
 // tuning and tests, validated by inspect.cu's exec_config).
 struct ExecCfg {
-  int32_t pf;          // L2 bulk prefetch bits (SABLE_XPREFETCH; inspect.cu exec_config)
+  int32_t pf;          // 1: bulk L2 prefetch of a warp batch's later units (SABLE_XPREFETCH)
   int32_t ustage;      // cap on one unit's bytes (SABLE_USTAGE; plan.cu)
   int32_t rem_rows;    // rows per remainder-only unit (SABLE_UREM_ROWS)
-  int32_t batch;       // units per warp batch (SABLE_UBATCH_UNITS)
+  int32_t batch;       // max units per warp batch (SABLE_UBATCH_UNITS)
+  int32_t batch_bytes; // bytes that close a warp batch (SABLE_UBATCH_BYTES)
   int32_t sliced;      // 1: world-1 exchange steps run the slice launches (SABLE_SLICED, tests)
-  int32_t exec;        // SpMV executor: 0 unit_kernel (batches), 1 wunit_kernel (SABLE_EXEC=unit|window)
-  int32_t unit_cost;   // windowed executor: per-unit overhead in bytes for the warp ranges (SABLE_UNIT_COST)
 };
 
 // ---- the unit executor (unit.cu, plan.cu)
@@ -105,7 +104,8 @@ static_assert(sizeof(XgU) == 16, "XgU is 16 B");
 #define SABLE_UNIT_WARPS 1  // A/B builds: warps per unit-executor CTA (1: measured r02)
 #endif
 constexpr int kUnitWarps = SABLE_UNIT_WARPS;
-constexpr int kUnitBytes = 32768;  // default cap on one unit's data (plan.cu), unit_kernel
+constexpr int kUnitBytes = 16384;  // default cap on one unit's data (plan.cu)
+constexpr int kBatchBytes = 8192;  // default bytes that close a warp batch (plan.cu)
 constexpr int kUnitBatch = 4;      // default units per warp batch
 constexpr int kSlices = 8;         // exchange slices of a shard (comm.cu overlap)
 
@@ -204,10 +204,6 @@ struct sable_handle {
   void* mma_scratch = nullptr;       // sable_spmm on the tensor cores: 128 partials per slot
   std::vector<int64_t> slice_batch;  // kSlices + 1 batch boundaries (host)
   std::vector<int64_t> slice_row;    // kSlices + 1 local row boundaries (host)
-  // windowed executor (unit.cu stage_setup): persistent grid of st_G warps,
-  // per-warp unit ranges for the whole shard and for each exchange slice
-  int32_t* st_wcut = nullptr;        // (1 + kSlices) * (st_G + 1)
-  int64_t st_G = 0;                  // 0: the windowed executor is off
 
   // export data (device): local cells and tile geometry
   int32_t* cell_br = nullptr;

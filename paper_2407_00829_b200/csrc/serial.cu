@@ -24,7 +24,6 @@
 namespace sable {
 
 void free_handle(sable_handle* h);
-cudaError_t stage_setup(sable_handle* h, const Unit* hu, const int32_t* hbatch);  // unit.cu
 
 namespace {
 
@@ -342,9 +341,9 @@ extern "C" sable_status sable_deserialize(const void* buf, int64_t size, void* c
       H.br_end > H.nbr || H.row_begin < 0 || H.row_end < H.row_begin || H.row_end > H.nrows ||
       H.nrows < 1 || H.ncols < 1 || H.nrows >= (1ll << 31) - 1 || H.ncols >= (1ll << 31) - 1)
     return fail(SABLE_E_FORMAT, "sable_deserialize: inconsistent header");
-  if (H.cfg.pf < 0 || H.cfg.pf > 3 || H.cfg.ustage < 1024 || H.cfg.ustage % 16 != 0 ||
+  if (H.cfg.pf < 0 || H.cfg.pf > 1 || H.cfg.ustage < 1024 || H.cfg.ustage % 16 != 0 ||
       H.cfg.ustage > (1 << 24) || H.cfg.rem_rows < 1 || H.cfg.rem_rows > 32 || H.cfg.batch < 1 ||
-      H.cfg.exec < 0 || H.cfg.exec > 1 || H.cfg.unit_cost < 0 || H.cfg.unit_cost > (1 << 24))
+      H.cfg.batch_bytes < 1)
     return fail(SABLE_E_FORMAT, "sable_deserialize: executor configuration out of range");
   {
     const int64_t lim = (int64_t)1 << 40;  // bounds every count so that byte sizes cannot wrap
@@ -430,10 +429,6 @@ extern "C" sable_status sable_deserialize(const void* buf, int64_t size, void* c
   dal((void**)&h->ucounters, 4 * h->n_uxg);
   if (!e) e = cudaMemsetAsync(h->ucounters, 0, 4 * (size_t)std::max<int64_t>(h->n_uxg, 1), st);
   if (!e) e = cudaStreamSynchronize(st);  // the host image may be released on return
-  // the persistent executors' per-warp unit ranges (device dependent: recomputed here)
-  if (!e)
-    e = stage_setup(h, reinterpret_cast<const Unit*>(in + offs[0]),
-                    reinterpret_cast<const int32_t*>(in + offs[1]));
   if (e) {
     set_error(cuda_msg(e, "sable_deserialize"));
     cudaStreamSynchronize(st);

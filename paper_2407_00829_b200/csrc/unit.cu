@@ -42,10 +42,6 @@
 // shard count or on timing), so y is bitwise reproducible and identical for
 // every P.
 #include <algorithm>
-#include <climits>
-#include <cstdlib>
-#include <string>
-#include <vector>
 
 #include "device.cuh"
 
@@ -350,132 +346,6 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
   }
 }
 
-// ---- the windowed executor (SABLE_EXEC=window)
-//
-// Persistent one-warp CTAs (every SM full at the kernel's occupancy), each
-// owning a contiguous range of units balanced by bytes at plan time
-// (stage_setup).  The warp's unit descriptors arrive in windows of 32 (1 KB
-// bulk copies into a double-buffered shared-memory window, the next window
-// in flight while the current one is used), so no unit waits on a descriptor
-// load, and every kPfGroup units lane 0 pulls the data of the next group of units
-// (contiguous ranges of the panels, x maps, remainder pointers, columns and
-// values) into L2 with bulk prefetches.  The per-unit arithmetic is
-// unit_kernel's (dense_rows, rem_rows, finish_unit), so y is bitwise the same.
-
-constexpr int kPfGroup = 4;
-constexpr int kWin = 32;  // unit descriptors per window
-
-// Lane 0: descriptors [w0, w0 + n) into window buffer `dst`, complete on `bar`.
-__device__ __forceinline__ void window_issue(const Unit* units, int32_t w0, int32_t n,
-                                             uint32_t dst, uint32_t bar) {
-  mbar_expect_tx(bar, (uint32_t)n * 32u);
-  bulk_g2s(dst, units + w0, (uint32_t)n * 32u, bar);
-}
-
-// Lanes i < n read window entry i; lane 0 pulls the window's x-map span and
-// remainder row-pointer span into L2 (two bulk prefetches per window: the
-// x map is the one dependent load in front of a unit's x gathers).
-template <typename T>
-__device__ __forceinline__ void window_maps_prefetch(const UPlan<T>& P, const Unit* w, int n,
-                                                     int lane) {
-  int qs = INT_MAX, qe = INT_MIN, rs = INT_MAX, re = INT_MIN;
-  if (lane < n) {
-    const Unit U = load_unit_smem(w + lane);
-    if (U.wq > 0) {
-      qs = U.xq0;
-      qe = U.xq0 + U.wq;
-    }
-    if (U.e1 > U.e0) {
-      rs = U.row0;
-      re = U.row0 + U.nr + 1;
-    }
-  }
-  qs = __reduce_min_sync(kFull, qs);
-  qe = __reduce_max_sync(kFull, qe);
-  rs = __reduce_min_sync(kFull, rs);
-  re = __reduce_max_sync(kFull, re);
-  if (lane == 0) {
-    if (qe > qs) l2_prefetch(P.xq + qs, (int64_t)(qe - qs) * (int64_t)sizeof(XMap));
-    if (re > rs) l2_prefetch(P.rptr + rs, (int64_t)(re - rs) * 4);
-  }
-}
-
-template <typename T, int KV>
-__global__ void __launch_bounds__(32, kUnitMinBlocks)
-    wunit_kernel(const __grid_constant__ UPlan<T> P, const int32_t* __restrict__ wcut,
-                 const T* __restrict__ x, T* __restrict__ y) {
-  __shared__ __align__(16) T buf_s[kRemWave * KV];
-  __shared__ __align__(128) Unit win[2][kWin];
-  __shared__ __align__(8) uint64_t wbar[2];
-  const int lane = threadIdx.x;
-  const int32_t u0 = __ldg(wcut + blockIdx.x), u1 = __ldg(wcut + blockIdx.x + 1);
-  if (u0 >= u1) return;
-  const uint32_t bar0 = smem_u32(&wbar[0]), win0 = smem_u32(&win[0][0]);
-  if (lane == 0) {
-    mbar_init(bar0, 1);
-    mbar_init(bar0 + 8, 1);
-    fence_mbar_init();
-    window_issue(P.units, u0, min(kWin, u1 - u0), win0, bar0);
-    if (u1 - u0 > kWin)
-      window_issue(P.units, u0 + kWin, min(kWin, u1 - u0 - kWin), win0 + kWin * 32, bar0 + 8);
-  }
-  __syncwarp();
-  int32_t base = u0;
-  int wb = 0;          // window buffer of [base, base + kWin)
-  uint32_t wph = 0;    // its phase
-  mbar_wait(bar0, 0);
-  if (P.pf & 2) window_maps_prefetch<T>(P, win[0], min(kWin, u1 - u0), lane);
-  if ((P.pf & 1) && lane == 0 && u1 - u0 > 1)
-    prefetch_span<T>(P, win[0][1], win[0][min(2 * kPfGroup - 1, min(kWin - 1, u1 - u0 - 1))]);
-  for (int32_t u = u0; u < u1; ++u) {
-    int j = u - base;
-    if (j == kWin) {  // window base is done: refill its buffer with base + 2 kWin
-      __syncwarp();
-      if (lane == 0 && base + 2 * kWin < u1) {
-        fence_proxy_async_smem();
-        window_issue(P.units, base + 2 * kWin, min(kWin, u1 - base - 2 * kWin),
-                     win0 + (uint32_t)(wb * kWin * 32), bar0 + 8u * wb);
-      }
-      base = u;
-      j = 0;
-      wb ^= 1;
-      if (wb == 0) wph ^= 1u;
-      mbar_wait(bar0 + 8u * wb, wph);
-    }
-    if ((P.pf & 2) && j == kWin / 2 && base + kWin < u1) {
-      // the next window's descriptors (in flight since this window began)
-      mbar_wait(bar0 + 8u * (wb ^ 1), wb == 0 ? wph : wph ^ 1u);
-      window_maps_prefetch<T>(P, win[wb ^ 1], min(kWin, u1 - base - kWin), lane);
-    }
-    const Unit U = load_unit_smem(&win[wb][j]);
-    if ((P.pf & 1) && lane == 0 && j % kPfGroup == 0) {
-      const int ja = j + kPfGroup, jb = min(min(j + 2 * kPfGroup - 1, kWin - 1), u1 - base - 1);
-      if (ja <= jb) prefetch_span<T>(P, win[wb][ja], win[wb][jb]);
-    }
-    T s[KV];
-#pragma unroll
-    for (int jj = 0; jj < KV; ++jj) s[jj] = T(0);
-    const int ne = U.e1 - U.e0;
-    int lo = 0, hi = 0;
-    if (ne > 0 && lane < U.nr) {
-      lo = max(__ldg(P.rptr + U.row0 + lane), U.e0);
-      hi = min(__ldg(P.rptr + U.row0 + lane + 1), U.e1);
-    }
-    if (U.wq > 0) {
-      switch (U.llpr) {
-        case 0: dense_rows<T, 1, KV>(P, U, x, lane, s); break;
-        case 1: dense_rows<T, 2, KV>(P, U, x, lane, s); break;
-        case 2: dense_rows<T, 4, KV>(P, U, x, lane, s); break;
-        case 3: dense_rows<T, 8, KV>(P, U, x, lane, s); break;
-        case 4: dense_rows<T, 16, KV>(P, U, x, lane, s); break;
-        default: dense_rows<T, 32, KV>(P, U, x, lane, s); break;
-      }
-    }
-    if (ne > 0) rem_rows<T, KV>(P, U, x, buf_s, lane, lo, hi, s);
-    finish_unit<T, KV>(P, U, s, y, lane);
-  }
-}
-
 template <typename T>
 UPlan<T> make_plan(const sable_handle* h, void* scratch) {
   UPlan<T> P;
@@ -511,84 +381,14 @@ cudaError_t launch_kv(const sable_handle* h, const void* x, void* y, void* scrat
   return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_window(const sable_handle* h, const void* x, void* y, cudaStream_t st,
-                          const int32_t* wcut) {
-  const UPlan<T> P = make_plan<T>(h, h->uscratch);
-  wunit_kernel<T, 1><<<(unsigned)h->st_G, 32, 0, st>>>(P, wcut, static_cast<const T*>(x),
-                                                        static_cast<T*>(y));
-  return cudaGetLastError();
-}
-
-// Per-warp unit ranges of the windowed executor: st_G persistent one-warp
-// CTAs (every SM full at the kernel's occupancy), each a contiguous range of
-// units of about equal cost (bytes + a per-unit overhead), for the whole
-// shard and for each exchange slice.
-template <typename T>
-cudaError_t stage_setup_t(sable_handle* h, const Unit* hu, const int32_t* hbatch) {
-  const void* fn = reinterpret_cast<const void*>(&wunit_kernel<T, 1>);
-  int occ = 0, nsm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32, 0);
-  if (!e) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
-  if (e) return e;
-  if (occ < 1) {
-    set_error("windowed executor: no resident CTA");
-    return cudaErrorInvalidValue;
-  }
-  const int64_t G = (int64_t)nsm * occ;
-  const int64_t kUnitCost = h->cfg.unit_cost;  // per-unit overhead in byte equivalents
-  const int64_t n = h->n_units;
-  std::vector<int64_t> pre((size_t)n + 1, 0);
-  for (int64_t i = 0; i < n; ++i) {
-    const Unit& U = hu[i];
-    const int64_t bytes = (int64_t)U.nr * U.wq * 16 + (int64_t)U.wq * (int64_t)sizeof(XMap) +
-                          (int64_t)(U.e1 - U.e0) * (4 + (int64_t)sizeof(T));
-    pre[i + 1] = pre[i] + bytes + kUnitCost;
-  }
-  std::vector<int32_t> cut((size_t)(1 + kSlices) * (G + 1));
-  auto fill = [&](int32_t* c, int64_t a, int64_t b) {
-    const int64_t tot = pre[b] - pre[a];
-    for (int64_t k = 0; k <= G; ++k) {
-      const int64_t target = pre[a] + (int64_t)((double)tot * (double)k / (double)G);
-      int64_t i = std::lower_bound(pre.begin() + a, pre.begin() + b + 1, target) - pre.begin();
-      c[k] = (int32_t)std::min(std::max(i, a), b);
-    }
-    c[0] = (int32_t)a;
-    c[G] = (int32_t)b;
-  };
-  fill(cut.data(), 0, n);
-  for (int s = 0; s < kSlices; ++s)
-    fill(cut.data() + (size_t)(1 + s) * (G + 1), hbatch[h->slice_batch[s]],
-         hbatch[h->slice_batch[s + 1]]);
-  if (h->st_wcut) cudaFree(h->st_wcut);
-  h->st_wcut = nullptr;
-  e = cudaMalloc(reinterpret_cast<void**>(&h->st_wcut), sizeof(int32_t) * cut.size());
-  if (!e) e = cudaMemcpy(h->st_wcut, cut.data(), sizeof(int32_t) * cut.size(), cudaMemcpyHostToDevice);
-  if (e) return e;
-  h->st_G = G;
-  return cudaSuccess;
-}
-
 }  // namespace
 
-cudaError_t stage_setup(sable_handle* h, const Unit* hu, const int32_t* hbatch) {
-  h->st_G = 0;
-  if (h->cfg.exec == 0) return cudaSuccess;
-  return h->dtype == SABLE_F64 ? stage_setup_t<double>(h, hu, hbatch)
-                               : stage_setup_t<float>(h, hu, hbatch);
-}
-
 int32_t exec_grid(const sable_handle* h) {
-  if (!h) return 0;
-  if (h->st_G > 0) return (int32_t)h->st_G;
-  return (int32_t)((h->n_ubatch + kUnitWarps - 1) / kUnitWarps);
+  return h ? (int32_t)((h->n_ubatch + kUnitWarps - 1) / kUnitWarps) : 0;
 }
 
 // y = A x (one launch).
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st) {
-  if (h->st_G > 0)
-    return h->dtype == SABLE_F64 ? launch_window<double>(h, x, y, st, h->st_wcut)
-                                 : launch_window<float>(h, x, y, st, h->st_wcut);
   return h->dtype == SABLE_F64 ? launch_kv<double, 1>(h, x, y, h->uscratch, st)
                                : launch_kv<float, 1>(h, x, y, h->uscratch, st);
 }
@@ -596,11 +396,6 @@ cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t
 // y rows of exchange slice s only (its warp batches; comm.cu).
 cudaError_t run_spmv_slice(const sable_handle* h, const void* x, void* y, int s,
                            cudaStream_t st) {
-  if (h->st_G > 0) {
-    const int32_t* wc = h->st_wcut + (size_t)(1 + s) * (h->st_G + 1);
-    return h->dtype == SABLE_F64 ? launch_window<double>(h, x, y, st, wc)
-                                 : launch_window<float>(h, x, y, st, wc);
-  }
   const int64_t b0 = h->slice_batch[s], b1 = h->slice_batch[s + 1];
   return h->dtype == SABLE_F64 ? launch_kv<double, 1>(h, x, y, h->uscratch, st, b0, b1)
                                : launch_kv<float, 1>(h, x, y, h->uscratch, st, b0, b1);
