@@ -38,8 +38,8 @@ def build(force: bool = False, verbose: bool = False, variant: str = "",
         return LIB
     inc, lib = _nccl_dirs()
     nvcc = os.environ.get("NVCC", "nvcc")
-    objs = []
     os.makedirs(bdir, exist_ok=True)
+    cmds, objs = [], []
     for s in srcs:
         o = os.path.join(bdir, os.path.basename(s) + ".o")
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
@@ -47,8 +47,12 @@ def build(force: bool = False, verbose: bool = False, variant: str = "",
                "-I", inc, *extra, "-c", s, "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
-        subprocess.check_call(cmd)
+        cmds.append(cmd)
         objs.append(o)
+    # one nvcc per source, in parallel (they are independent translation units)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+        list(ex.map(subprocess.check_call, cmds))
     cmd = [nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-L", lib, "-l:libnccl.so.2",
            "-Xlinker", "-rpath=" + lib, "-lcudart"]
     subprocess.check_call(cmd)

@@ -536,7 +536,7 @@ int64_t env_int(const char* name, int64_t dflt) {
 // defaults (tuning runs and tests).  Invalid overrides -> SABLE_E_INVALID_ARG.
 ExecCfg exec_config() {
   ExecCfg c{};
-  c.pf = (int32_t)env_int("SABLE_XPREFETCH", 1);
+  c.pf = (int32_t)env_int("SABLE_XPREFETCH", 0);
   c.ustage = (int32_t)env_int("SABLE_USTAGE", kUnitBytes);
   c.rem_rows = (int32_t)env_int("SABLE_UREM_ROWS", 32);
   c.batch = (int32_t)env_int("SABLE_UBATCH_UNITS", kUnitBatch);

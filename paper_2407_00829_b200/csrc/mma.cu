@@ -90,6 +90,7 @@ __device__ __forceinline__ float tf32_rna(float v) {
 
 // Global column of panel column f of a unit (x map entry of its 4-column vector).
 __device__ __forceinline__ int panel_col(const UPlan<float>& P, int xq0, int f) {
+  SABLE_DCHECK(xq0 + (f >> 2) < P.n_xq);
   const XMap m = ldg_xmap(P.xq + xq0 + (f >> 2));
   const int i = f & 3;
   if (m.c >= 0) {
@@ -232,6 +233,7 @@ __global__ void __launch_bounds__(kMmaThreads, 1)
       const int4 gv = __ldg(reinterpret_cast<const int4*>(P.xg + U.xg));
       const int64_t slot = (int64_t)(((uint64_t)(uint32_t)gv.y << 32) | (uint32_t)gv.x);
       const int counter = gv.z, np = gv.w;
+      SABLE_DCHECK(slot >= 0 && (slot + (int64_t)np * kN) * kM <= P.scratch_elems);
       float* sp = P.scratch + slot * kM;
       if (m < k)
         for (int n = 0; n < nr; ++n) __stcg(sp + (U.piece * 32 + n) * kM + m, S.yt[n * kM + m]);
@@ -281,6 +283,7 @@ cudaError_t run_spmm_mma(const sable_handle* h, const void* X, void* Y, int32_t 
   P.b0 = 0;
   P.n_batches = h->n_ubatch;
   P.pf = 0;
+  plan_extents<float>(P, h, h->uscratch_slots * (int64_t)kM);
   int dev = 0, sms = 148;
   cudaError_t e = cudaGetDevice(&dev);
   if (!e) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -311,6 +311,16 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
     }
     while ((int)ucut.size() < kSlices + 1) ucut.push_back((int64_t)U.size());
   }
+  // units per batch: at most batch_units, fewer when the shard has too few
+  // units to give every resident warp slot (SMs x 32) about two batches
+  int64_t bu = B.batch_units;
+  {
+    int nsm = 148;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess)
+      nsm = 148;
+    const int64_t slots = 2ll * nsm * 32;
+    bu = std::max<int64_t>(1, std::min<int64_t>(bu, (int64_t)U.size() / slots));
+  }
   std::vector<int32_t> batch;
   h->slice_batch.assign(kSlices + 1, 0);
   h->slice_row.assign(kSlices + 1, 0);
@@ -324,7 +334,7 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
     for (int64_t i = ucut[s]; i < ucut[s + 1]; ++i) {
       if (nb == 0) batch.push_back((int32_t)i);
       bb += (int64_t)U[i].nr * U[i].wq * 16 + (int64_t)(U[i].e1 - U[i].e0) * ent + 64;
-      if (++nb >= B.batch_units || bb >= B.batch_bytes) nb = bb = 0;
+      if (++nb >= bu || bb >= B.batch_bytes) nb = bb = 0;
     }
   }
   h->slice_batch[kSlices] = (int64_t)batch.size();

@@ -124,7 +124,27 @@ struct UPlan {
   int32_t* counters;
   int64_t b0, n_batches;  // batches [b0, n_batches) of this launch
   int32_t pf;             // 1: bulk L2 prefetch of the next unit's data
+  // array extents, read only by the bounds-checked build (SABLE_CHECKED)
+  int64_t n_units, pv_vecs, n_xq, n_xside, rem_nnz, nloc, ncols, n_uxg, scratch_elems;
 };
+
+// Bounds-checked build (build.py variant "checked", -DSABLE_CHECKED): every
+// index the executors follow is checked on the device and a violation traps
+// (cudaErrorLaunchFailure), the pool's stand-in for compute-sanitizer.
+#ifdef SABLE_CHECKED
+#define SABLE_DCHECK(cond) \
+  do {                     \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define SABLE_DCHECK(cond) \
+  do {                     \
+  } while (0)
+#endif
+
+// Host side: fill the extents of a plan from its handle.
+template <typename T>
+inline void plan_extents(UPlan<T>& P, const sable_handle* h, int64_t scratch_elems);
 
 // Position of element (r, c) of a tile whose first panel column is cs, in a
 // row-major panel of width W at base pb (rows padded to 16 bytes).
@@ -242,3 +262,18 @@ struct sable_handle {
   int64_t bytes_alg = 0;
   double inspect_ms = 0.0;
 };
+
+namespace sable {
+template <typename T>
+inline void plan_extents(UPlan<T>& P, const sable_handle* h, int64_t scratch_elems) {
+  P.n_units = h->n_units;
+  P.pv_vecs = h->pv_elems * (int64_t)sizeof(T) / 16;
+  P.n_xq = h->n_xq;
+  P.n_xside = h->n_xside;
+  P.rem_nnz = h->rem_nnz;
+  P.nloc = h->row_end - h->row_begin;
+  P.ncols = h->ncols;
+  P.n_uxg = h->n_uxg;
+  P.scratch_elems = scratch_elems;
+}
+}  // namespace sable

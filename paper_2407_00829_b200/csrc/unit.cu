@@ -88,9 +88,15 @@ __device__ __forceinline__ void load_xv(const UPlan<T>& P, XMap m, const T* __re
   if (m.c >= 0) {
     const int k = m.kd & 3, d = m.kd >> 2;  // k = 0: d = 0
 #pragma unroll
-    for (int i = 0; i < N; ++i) ldg_kv<T, KV>(x + (int64_t)(m.c + i + (i >= k ? d : 0)) * KV, xv[i]);
+    for (int i = 0; i < N; ++i) {
+      SABLE_DCHECK(m.c + i + (i >= k ? d : 0) >= 0 && m.c + i + (i >= k ? d : 0) < P.ncols);
+      ldg_kv<T, KV>(x + (int64_t)(m.c + i + (i >= k ? d : 0)) * KV, xv[i]);
+    }
   } else {
+    SABLE_DCHECK(~m.c < P.n_xside);
     const int4 c = __ldg(P.xside + ~m.c);
+    SABLE_DCHECK(c.x >= 0 && c.x < P.ncols && c.y >= 0 && c.y < P.ncols);
+    SABLE_DCHECK(N == 2 || (c.z >= 0 && c.z < P.ncols && c.w >= 0 && c.w < P.ncols));
     ldg_kv<T, KV>(x + (int64_t)c.x * KV, xv[0]);
     ldg_kv<T, KV>(x + (int64_t)c.y * KV, xv[1]);
     if constexpr (N == 4) {
@@ -233,7 +239,10 @@ __device__ __forceinline__ void rem_rows(const UPlan<T>& P, const Unit& U,
       T xg[KV];
 #pragma unroll
       for (int j = 0; j < KV; ++j) xg[j] = T(0);
-      if (k * 32 + lane < n) ldg_kv<T, KV>(x + (int64_t)w.c[k] * KV, xg);
+      if (k * 32 + lane < n) {
+        SABLE_DCHECK(w.c[k] >= 0 && w.c[k] < P.ncols);
+        ldg_kv<T, KV>(x + (int64_t)w.c[k] * KV, xg);
+      }
 #pragma unroll
       for (int j = 0; j < KV; ++j) pr[k][j] = w.v[k] * xg[j];
     }
@@ -274,6 +283,7 @@ template <typename T, int KV>
 __device__ __forceinline__ void finish_unit(const UPlan<T>& P, const Unit& U, const T (&s)[KV],
                                             T* __restrict__ y, int lane) {
   if (U.xg < 0) {
+    SABLE_DCHECK(U.row0 >= 0 && U.row0 + U.nr <= P.nloc);
     if (lane < U.nr)
 #pragma unroll
       for (int j = 0; j < KV; ++j) y[(int64_t)(U.row0 + lane) * KV + j] = s[j];
@@ -282,6 +292,8 @@ __device__ __forceinline__ void finish_unit(const UPlan<T>& P, const Unit& U, co
   const int4 gv = __ldg(reinterpret_cast<const int4*>(P.xg + U.xg));
   const int64_t slot = (int64_t)(((uint64_t)(uint32_t)gv.y << 32) | (uint32_t)gv.x);
   const int counter = gv.z, np = gv.w;
+  SABLE_DCHECK(U.xg < P.n_uxg && counter >= 0 && counter < P.n_uxg && U.piece < np &&
+               slot >= 0 && (slot + (int64_t)np * 32) * KV <= P.scratch_elems);
   T* sp = P.scratch + slot * KV;
   if (lane < U.nr)
 #pragma unroll
@@ -318,9 +330,15 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
     const Unit Ul = load_unit(P.units + u1 - 1);
     if (lane == 0) prefetch_span<T>(P, Un, Ul);
   }
+  SABLE_DCHECK(u0 >= 0 && u0 <= u1 && u1 <= P.n_units);
   for (int u = u0; u < u1; ++u) {
     const Unit U = Un;
     if (u + 1 < u1) Un = load_unit(P.units + u + 1);
+    SABLE_DCHECK(U.nr >= 1 && U.nr <= 32 && U.llpr <= 5 && U.row0 >= 0 && U.row0 + U.nr <= P.nloc);
+    SABLE_DCHECK(U.wq == 0 || (U.wq > 0 && U.voff16 >= 0 &&
+                               (int64_t)U.voff16 + (int64_t)U.nr * U.wq <= P.pv_vecs &&
+                               U.xq0 >= 0 && (int64_t)U.xq0 + U.wq <= P.n_xq));
+    SABLE_DCHECK(U.e0 >= 0 && U.e0 <= U.e1 && U.e1 <= P.rem_nnz);
     T s[KV];
 #pragma unroll
     for (int j = 0; j < KV; ++j) s[j] = T(0);
@@ -363,6 +381,7 @@ UPlan<T> make_plan(const sable_handle* h, void* scratch) {
   P.b0 = 0;
   P.n_batches = h->n_ubatch;
   P.pf = h->cfg.pf;
+  plan_extents<T>(P, h, 0);
   return P;
 }
 
@@ -373,6 +392,7 @@ cudaError_t launch_kv(const sable_handle* h, const void* x, void* y, void* scrat
   if (b1 < 0) b1 = h->n_ubatch;
   if (b1 <= b0) return cudaSuccess;
   UPlan<T> P = make_plan<T>(h, scratch);
+  P.scratch_elems = h->uscratch_slots * (scratch == h->uscratch ? 1 : KV);
   P.b0 = b0;
   P.n_batches = b1;
   const int64_t blocks = (b1 - b0 + kUnitWarps - 1) / kUnitWarps;
