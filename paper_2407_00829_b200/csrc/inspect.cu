@@ -542,10 +542,11 @@ ExecCfg exec_config() {
   c.batch = (int32_t)env_int("SABLE_UBATCH_UNITS", kUnitBatch);
   c.batch_bytes = (int32_t)env_int("SABLE_UBATCH_BYTES", kBatchBytes);
   c.sliced = env_int("SABLE_SLICED", 0) != 0 ? 1 : 0;
+  c.lpr_mode = (int32_t)env_int("SABLE_LPR", 0);
   const int64_t arch = env_int("SABLE_ARCH", 2);
   if (arch != 2 || c.ustage < 1024 || c.ustage % 16 != 0 || c.ustage > (1 << 24) ||
       c.rem_rows < 1 || c.rem_rows > 32 || c.batch < 1 || (c.pf != 0 && c.pf != 1) ||
-      c.batch_bytes < 1) {
+      c.batch_bytes < 1 || c.lpr_mode < 0 || c.lpr_mode > 1) {
     set_error("invalid SABLE_ARCH / SABLE_USTAGE / SABLE_UREM_ROWS / SABLE_UBATCH_UNITS / "
               "SABLE_UBATCH_BYTES / SABLE_XPREFETCH (arch 2 only; ustage a multiple of 16 in "
               "[1024, 2^24]; 1..32 rows; batch >= 1; batch bytes >= 1)");

@@ -63,11 +63,17 @@ UnitBudget unit_budget(const ExecCfg& c) {
   return b;
 }
 
-// Lanes per row for a panel of wq column vectors: the smallest power of two
-// covering the panel in one pass, capped at 32.
-int choose_llpr(int64_t wq) {
+// Lanes per row for a panel of wq column vectors: mode 0 -- the smallest
+// power of two covering the panel in one pass; mode 1 -- the largest power of
+// two not above wq (every lane busy, several passes over the columns, more
+// rows per unit); both capped at 32.
+int choose_llpr(int64_t wq, int mode) {
   int l = 0;
-  while (l < 5 && (1ll << l) < wq) ++l;
+  if (mode == 1) {
+    while (l < 5 && (2ll << l) <= wq) ++l;
+  } else {
+    while (l < 5 && (1ll << l) < wq) ++l;
+  }
   return l;
 }
 
@@ -236,7 +242,7 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
     const int64_t xm_b = cover(wq * (int64_t)sizeof(XMap));
     if (row_b + xm_b + rp_bytes(1) + 64 + ent <= S) {
       // row groups: as many rows as the lanes' accumulators and a stage hold
-      const int llpr = choose_llpr(wq);
+      const int llpr = choose_llpr(wq, h->cfg.lpr_mode);
       const int64_t L = 1ll << llpr;
       const int64_t ru = std::min<int64_t>(32, (32 / L) * std::min<int64_t>(L, 8));
       const int64_t rs = std::max<int64_t>(1, (S - xm_b - rp_bytes(32) - 64 - ent) / row_b);
@@ -275,7 +281,7 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
           u.wq = (int32_t)n;
           u.xq0 = xq0 + (int32_t)qa;
           u.voff16 = (int32_t)(vbase + (int64_t)r * wq + qa);
-          u.llpr = (uint8_t)choose_llpr(n);
+          u.llpr = (uint8_t)choose_llpr(n, h->cfg.lpr_mode);
           u.e0 = u.e1 = H_rp[r0 + r];
           pieces.push_back(u);
         }

@@ -53,6 +53,7 @@ struct ExecCfg {
   int32_t batch;       // max units per warp batch (SABLE_UBATCH_UNITS)
   int32_t batch_bytes; // bytes that close a warp batch (SABLE_UBATCH_BYTES)
   int32_t sliced;      // 1: world-1 exchange steps run the slice launches (SABLE_SLICED, tests)
+  int32_t lpr_mode;    // lanes per row: 0 cover the panel in one pass, 1 largest power of two <= wq (SABLE_LPR)
 };
 
 // ---- the unit executor (unit.cu, plan.cu)

@@ -343,7 +343,7 @@ extern "C" sable_status sable_deserialize(const void* buf, int64_t size, void* c
     return fail(SABLE_E_FORMAT, "sable_deserialize: inconsistent header");
   if (H.cfg.pf < 0 || H.cfg.pf > 1 || H.cfg.ustage < 1024 || H.cfg.ustage % 16 != 0 ||
       H.cfg.ustage > (1 << 24) || H.cfg.rem_rows < 1 || H.cfg.rem_rows > 32 || H.cfg.batch < 1 ||
-      H.cfg.batch_bytes < 1)
+      H.cfg.batch_bytes < 1 || H.cfg.lpr_mode < 0 || H.cfg.lpr_mode > 1)
     return fail(SABLE_E_FORMAT, "sable_deserialize: executor configuration out of range");
   {
     const int64_t lim = (int64_t)1 << 40;  // bounds every count so that byte sizes cannot wrap

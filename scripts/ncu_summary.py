@@ -27,6 +27,8 @@ KEYS = [
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
     "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
     "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+    "smsp__inst_executed.sum",
 ]
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6,
         "usecond": 1e-6, "nsecond": 1e-9, "ms": 1e-3, "msecond": 1e-3}
@@ -84,6 +86,12 @@ def main():
                 # one SpMV = the captured launches of one step: sum them
                 traffic[cfg] = traffic.get(cfg, 0) + int(rd + wr)
                 lines.append(f"- traffic (read+write): {int(rd + wr)} B")
+            l2s = num(k, "lts__t_sectors_srcunit_tex_op_read.sum")
+            if l2s is not None and rd:
+                # L1 -> L2 read sectors (32 B) per DRAM byte read: > 1 means
+                # the kernel's reads are served from L2 more than once (the
+                # remainder's x gathers: 4 useful bytes per 32-byte sector)
+                lines.append(f"- L2 read sectors x 32 B / DRAM bytes read: {l2s * 32 / rd:.2f}")
             stalls = sorted(((float(v[0]), kk) for kk, v in k.items()
                              if kk.startswith("smsp__pcsamp_warps_issue_stalled_")
                              and not kk.endswith("_not_issued") and v[0] not in ("",)),
