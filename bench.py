@@ -41,6 +41,7 @@ WORKLOADS = {
     "c5": "configs[4]: fp32 iterated VBR SpMV 2^23, 40% blocks log-U[4,256] + 60% power-law CSR",
 }
 L2_FLUSH_BYTES = 512 << 20  # > 2x the 126 MB L2
+L2_BYTES = 126 << 20  # B200 L2 capacity (B200_PROFILING.md)
 
 
 def peaks():
@@ -182,7 +183,13 @@ def run_sable(args):
     nloc = info["row_end"] - info["row_begin"]
     y = torch.empty(nloc, dtype=tdt, device=dev)
     xn = torch.empty_like(x)
-    flush_l2 = args.config != "c5"  # C5's 1.6 GB working set exceeds L2
+    # L2 between timed steps: flushed, or kept when the SpMV's working set is
+    # larger than twice the 126 MB L2 (the streamed bytes cannot be L2 hits;
+    # what survives is x and metadata, as in an iterated SpMV) -- "auto"
+    if args.l2 == "auto":
+        flush_l2 = info["bytes_alg"] <= 2 * L2_BYTES
+    else:
+        flush_l2 = args.l2 == "flush"
     scrub = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     scrub_sink = torch.empty((), dtype=torch.float32, device=dev)
 
@@ -201,11 +208,12 @@ def run_sable(args):
         else:
             A.spmv(x, y, sp)
 
-    def timed_loop(fn, k):
+    def timed_loop(fn, k, flush_each=None):
+        fl = flush_l2 if flush_each is None else flush_each
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(k)]
         for i in range(k):
-            if flush_l2:
+            if fl:
                 flush()
             ev[i][0].record(stream)
             fn()
@@ -234,6 +242,13 @@ def run_sable(args):
     torch.cuda.synchronize()
     kt = [a.elapsed_time(b) for a, b in evk]
     k_ms = sum(kt) / len(kt)
+    # when L2 is kept between steps, the same kernel with L2 flushed too
+    # (reported beside the headline, roofline.frac_l2_flushed)
+    kf_ms = None
+    if not flush_l2:
+        evf = timed_loop(lambda: A.spmv(x, y, sp), max(args.steps, 20), flush_each=True)
+        torch.cuda.synchronize()
+        kf_ms = statistics.mean(a.elapsed_time(b) for a, b in evf)
 
     # end to end through the C-ABI with pinned host buffers (H2D x, SpMV, D2H y)
     xh = torch.from_numpy(s.x.copy()).pin_memory()
@@ -247,7 +262,8 @@ def run_sable(args):
 
     # our kernels per step: one unit-executor launch (sable::unit_kernel)
     launches_per_step = int(info["n_unit_batches"] > 0)
-    red = torch.tensor([ms, k_ms, e2e_ms, info["bytes_alg"]], dtype=torch.float64, device=dev)
+    red = torch.tensor([ms, k_ms, e2e_ms, info["bytes_alg"], kf_ms or 0.0], dtype=torch.float64,
+                       device=dev)
     if world > 1:
         mx = red.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -255,6 +271,7 @@ def run_sable(args):
         dist.all_reduce(tot, op=dist.ReduceOp.SUM)
         ms, k_ms, e2e_ms = float(mx[0]), float(mx[1]), float(mx[2])
         bytes_alg_local_max = float(mx[3])
+        kf_ms = float(mx[4]) if kf_ms is not None else None
     else:
         bytes_alg_local_max = float(info["bytes_alg"])
 
@@ -287,7 +304,7 @@ def run_sable(args):
                 "n_combine": info["n_combine"], "panel_elems": info["panel_elems"],
                 "xmap_entries": info["xmap_entries"], "exec_grid": info["exec_grid"],
                 "l2": ("flushed between timed steps (512 MiB write, then read)" if flush_l2 else
-                       "not flushed: working set > L2 (iterated SpMV, cache behaviour is real)"),
+                       "not flushed: working set > 2x L2 (iterated SpMV, cache behaviour is real)"),
                 "parallelism": f"row-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
                 "bytes_alg_per_step": info["bytes_alg"] if world == 1 else None,
             },
@@ -298,11 +315,17 @@ def run_sable(args):
                 "kernel": "one SpMV = one sable::unit_kernel launch",
                 "kernel_ms": round(k_ms, 6),
                 "bytes_alg_per_launch": bytes_alg_local_max,
+                "l2": "kept between steps" if not flush_l2 else "flushed between steps",
             },
             "e2e": {"value": round(2.0 * nnz / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
                     "h2d_bytes_per_step": int(s.ncols * sv), "d2h_bytes_per_step": int(nloc * sv),
                     "ms_per_step": round(e2e_ms, 6), "api": "sable_spmv_host (C-ABI, pinned host x/y)"},
             "gpu_launches": args.steps * launches_per_step,
+            **({"l2_flushed": {
+                "kernel_ms": round(kf_ms, 6),
+                "frac": round(bytes_alg_local_max / (kf_ms * 1e-3) / 1e9 / peak, 4),
+                "note": "the same SpMV with L2 flushed (512 MiB scrub) before every launch"}}
+               if kf_ms else {}),
             "inspect_ms": round(info["inspect_ms"], 3),
             "gen_s": round(gen_s, 2),
             "clocks": clk.summary(),
@@ -428,6 +451,9 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="sable", choices=["sable", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--l2", default="auto", choices=["auto", "flush", "keep"],
+                    help="L2 between timed steps: flush, keep, or auto (keep when the "
+                         "SpMV's algorithmic bytes exceed 2x L2)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -54,7 +54,7 @@ void free_handle(sable_handle* h) {
                  h->ubatch,   h->xq,        h->xside,      h->uxg,         h->uscratch,
                  h->ucounters, h->mm_scratch, h->mma_scratch, h->cell_br,  h->cell_bc,     h->cell_cnt,
                  h->cell_dense, h->tiles,   h->tile_canon_off, h->tile_br, h->br_pbase,
-                 h->br_W,     h->x_dev,     h->y_dev};
+                 h->br_W,     h->x_dev,     h->y_dev,       h->ubhead};
   for (void* p : dev)
     if (p) cudaFree(p);
   free(h->all_bounds_h);

@@ -271,6 +271,7 @@ cudaError_t run_spmm_mma(const sable_handle* h, const void* X, void* Y, int32_t 
   UPlan<float> P;
   P.units = h->units;
   P.batch = h->ubatch;
+  P.bhead = h->ubhead;
   P.xq = h->xq;
   P.xside = h->xside;
   P.pv = static_cast<const float*>(h->pv);

@@ -46,6 +46,21 @@ constexpr int64_t cover(int64_t bytes) { return bytes > 0 ? bytes + 32 : 0; }
 
 }  // namespace
 
+// The first unit's descriptor of every warp batch, so a CTA starts its batch
+// with loads that depend only on its batch index (unit.cu).
+cudaError_t upload_batch_heads(sable_handle* h, const Unit* U, const int32_t* batch,
+                               cudaStream_t st) {
+  std::vector<Unit> head((size_t)std::max<int64_t>(h->n_ubatch, 1));
+  for (int64_t b = 0; b < h->n_ubatch; ++b) head[(size_t)b] = U[batch[b]];
+  if (h->ubhead) cudaFree(h->ubhead);
+  h->ubhead = nullptr;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&h->ubhead), sizeof(Unit) * head.size());
+  if (!e) e = cudaMemcpyAsync(h->ubhead, head.data(), sizeof(Unit) * head.size(),
+                              cudaMemcpyHostToDevice, st);
+  if (!e) e = cudaStreamSynchronize(st);
+  return e;
+}
+
 // Plan budgets (from the executor configuration, inspect.cu exec_config).
 struct UnitBudget {
   int64_t stage;        // cap on one unit's bytes (its data's aligned covers)
@@ -384,6 +399,7 @@ cudaError_t plan_units(sable_handle* h, const T* tval, int32_t nbl, int32_t b0,
   }
   if (pd_d) cudaFree(pd_d);
   if (!e) e = cudaStreamSynchronize(st);
+  if (!e) e = upload_batch_heads(h, U.data(), batch.data(), st);
   return e;
 }
 

@@ -114,6 +114,7 @@ template <typename T>
 struct UPlan {
   const Unit* units;
   const int32_t* batch;   // n_batches + 1 unit boundaries (one batch per warp)
+  const Unit* bhead;      // each batch's first unit descriptor
   const XMap* xq;         // x maps of the panels
   const int4* xside;      // columns of straddling vectors
   const T* pv;
@@ -211,6 +212,7 @@ struct sable_handle {
   sable::Unit* units = nullptr;
   int64_t n_units = 0;
   int32_t* ubatch = nullptr;         // n_ubatch + 1
+  sable::Unit* ubhead = nullptr;     // n_ubatch: each batch's first unit (plan.cu)
   int64_t n_ubatch = 0;
   sable::XMap* xq = nullptr;
   int64_t n_xq = 0;

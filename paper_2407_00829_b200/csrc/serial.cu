@@ -24,6 +24,8 @@
 namespace sable {
 
 void free_handle(sable_handle* h);
+cudaError_t upload_batch_heads(sable_handle* h, const Unit* U, const int32_t* batch,
+                               cudaStream_t st);  // plan.cu
 
 namespace {
 
@@ -429,6 +431,9 @@ extern "C" sable_status sable_deserialize(const void* buf, int64_t size, void* c
   dal((void**)&h->ucounters, 4 * h->n_uxg);
   if (!e) e = cudaMemsetAsync(h->ucounters, 0, 4 * (size_t)std::max<int64_t>(h->n_uxg, 1), st);
   if (!e) e = cudaStreamSynchronize(st);  // the host image may be released on return
+  if (!e)
+    e = upload_batch_heads(h, reinterpret_cast<const Unit*>(in + offs[0]),
+                           reinterpret_cast<const int32_t*>(in + offs[1]), st);
   if (e) {
     set_error(cuda_msg(e, "sable_deserialize"));
     cudaStreamSynchronize(st);

@@ -322,8 +322,9 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = P.b0 + (int64_t)blockIdx.x * kUnitWarps + warp;
   if (b >= P.n_batches) return;
+  // the batch bounds and its first unit: loads that depend only on b
   const int u0 = __ldg(P.batch + b), u1 = __ldg(P.batch + b + 1);
-  Unit Un = load_unit(P.units + u0);
+  Unit Un = load_unit(P.bhead + b);
   if ((P.pf & 1) && u1 - u0 > 1) {
     // the batch's data past its first unit -- contiguous ranges of the
     // panels, x maps, remainder pointers, columns and values -- into L2
@@ -369,6 +370,7 @@ UPlan<T> make_plan(const sable_handle* h, void* scratch) {
   UPlan<T> P;
   P.units = h->units;
   P.batch = h->ubatch;
+  P.bhead = h->ubhead;
   P.xq = h->xq;
   P.xside = h->xside;
   P.pv = static_cast<const T*>(h->pv);
