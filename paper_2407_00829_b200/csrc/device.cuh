@@ -157,8 +157,22 @@ __device__ __forceinline__ Unit load_unit_smem(const void* p) {
   return unpack_unit(q[0], q[1]);
 }
 
+// Loads of data read by many units (x maps and x): non-coherent, with an L2
+// evict_last policy so the streamed panel values and remainder entries
+// (evict_first) do not push them out of L2, within one SpMV and between the
+// steps of an iterated one (measured: C4 0.0854 -> 0.0826 ms with L2 flushed
+// before every SpMV, C3 0.0612 -> 0.0595 ms).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 __device__ __forceinline__ XMap ldg_xmap(const XMap* p) {
-  const int2 v = __ldg(reinterpret_cast<const int2*>(p));
+  int2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+      : "=r"(v.x), "=r"(v.y)
+      : "l"(p), "l"(policy_evict_last()));
   return XMap{v.x, v.y};
 }
 
@@ -167,7 +181,15 @@ __device__ __forceinline__ XMap ldg_xmap(const XMap* p) {
 template <typename T, int KV>
 __device__ __forceinline__ void ldg_kv(const T* __restrict__ p, T (&o)[KV]) {
   if constexpr (KV == 1) {
-    o[0] = __ldg(p);
+    if constexpr (sizeof(T) == 4) {
+      float v;
+      asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(policy_evict_last()));
+      o[0] = v;
+    } else {
+      double v;
+      asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(policy_evict_last()));
+      o[0] = v;
+    }
   } else if constexpr (sizeof(T) * KV >= 16) {
     using V = typename Vec<T>::V;
     constexpr int N = Vec<T>::N;
