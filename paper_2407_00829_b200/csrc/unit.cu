@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
   const int64_t b = P.b0 + (int64_t)blockIdx.x * kUnitWarps + warp;
   if (b >= P.n_batches) return;
   // the batch bounds and its first unit: loads that depend only on b
-  const int u0 = __ldg(P.batch + b), u1 = __ldg(P.batch + b + 1);
+  const int u0 = ldg_meta(P.batch + b), u1 = ldg_meta(P.batch + b + 1);
   Unit Un = load_unit(P.bhead + b);
   if ((P.pf & 1) && u1 - u0 > 1) {
     // the batch's data past its first unit -- contiguous ranges of the
@@ -347,8 +347,8 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
     const int ne = U.e1 - U.e0;
     int lo = 0, hi = 0;
     if (ne > 0 && lane < U.nr) {
-      lo = max(__ldg(P.rptr + U.row0 + lane), U.e0);
-      hi = min(__ldg(P.rptr + U.row0 + lane + 1), U.e1);
+      lo = max(ldg_meta(P.rptr + U.row0 + lane), U.e0);
+      hi = min(ldg_meta(P.rptr + U.row0 + lane + 1), U.e1);
     }
     if (U.wq > 0) {
       switch (U.llpr) {
