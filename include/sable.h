@@ -274,6 +274,37 @@ sable_status sable_spmv_allgather(sable_handle* h, const void* x_full, void* x_n
 sable_status sable_spmv_iterate(sable_handle* h, void* x_a, void* x_b, int32_t iters,
                                 void* cuda_stream, int32_t* result_in_b);
 
+/* ---- fused exchange epilogue (north_star s7) ------------
+ * Iterated SpMV ping-pongs two full x buffers.  Once they
+ * are registered with the handle, an exchange step whose x_next is one of
+ * them is ONE kernel launch: the SpMV's epilogue stores every finished y row
+ * into the local x_next and into the same row of every peer's x_next through
+ * NVLink peer mappings, so no broadcast follows the SpMV; the step ends with
+ * a one-word ncclAllReduce as the barrier (all rows have landed here; every
+ * rank is done reading the buffer the next step overwrites).  y is bitwise
+ * the same as on the NCCL path.  Steps on unregistered buffers keep using the
+ * NCCL broadcast pipeline.  At most 8 ranks.
+ *
+ * sable_comm_fuse: x_a, x_b are device buffers (ncols values each) inside
+ *   cudaMalloc allocations (CUDA IPC: not cudaMallocAsync / VMM memory), one
+ *   process per GPU, after sable_comm_init; collective (every rank calls it):
+ *   the allocations' IPC handles are all-gathered and every peer's buffers
+ *   mapped (SABLE_E_CUDA if peer access is unavailable).  world == 1: no
+ *   peers, the step is the plain SpMV.
+ * sable_comm_set_peers: the caller supplies the mappings itself (peers_a[q],
+ *   peers_b[q]: peer q's x_a / x_b as device pointers valid on this GPU, from
+ *   its own symmetric-memory or IPC setup; host arrays of npeers <= 7
+ *   pointers, copied).  With a communicator the step barrier is the
+ *   all-reduce above; without one (sable_comm_init not called) the caller
+ *   orders the ranks' steps itself (e.g. all ranks of a test on one stream).
+ * sable_comm_unfuse: forget the registration (unmaps IPC mappings).
+ * The buffers must stay allocated while registered; sable_destroy and
+ * sable_comm_init unfuse. */
+sable_status sable_comm_fuse(sable_handle* h, void* x_a, void* x_b);
+sable_status sable_comm_set_peers(sable_handle* h, void* x_a, void* x_b,
+                                  void* const* peers_a, void* const* peers_b, int32_t npeers);
+sable_status sable_comm_unfuse(sable_handle* h);
+
 /* The all-gather layout on the host (no device work): for per-block-row
  * weights (as in sable_shard_bounds) and the row grid rpntr[nbrows+1], the
  * global row bounds of every rank's slice of y, row_bounds[world+1]

@@ -12,6 +12,18 @@
 // (serialized vs overlapped bound).  Every rank's slice row
 // bounds are all-gathered once at sable_comm_init.
 //
+// Fused exchange epilogue.  Once the two ping-pong x
+// buffers are registered (sable_comm_fuse: their CUDA IPC handles are
+// all-gathered and every peer's buffers mapped over NVLink;
+// sable_comm_set_peers: the caller supplies the peer mappings), a step is ONE
+// unit-kernel launch whose epilogue stores each finished y row into its own
+// x_next and into the same row of every peer's x_next (st.global through the
+// peer mapping), so the transfer rides along with the SpMV row by row and no
+// broadcast follows.  The step ends with a barrier (a one-word ncclAllReduce
+// on the caller's stream): after it every rank's rows have landed in this
+// rank's x_next, and every rank has finished reading the buffer the next
+// step overwrites.
+//
 // sable_spmv_iterate runs `iters` steps ping-ponging two x buffers as ONE
 // CUDA graph (captured once per (x_a, x_b, iters), relaunched afterwards; the
 // NCCL calls are captured with the kernels) on an internal stream joined to
@@ -31,6 +43,8 @@ namespace sable {
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st);
 cudaError_t run_spmv_slice(const sable_handle* h, const void* x, void* y, int s,
                            cudaStream_t st);
+cudaError_t run_spmv_fused(const sable_handle* h, const void* x, void* y, void* const* peers,
+                           int npeer, cudaStream_t st);
 
 namespace {
 
@@ -69,12 +83,45 @@ sable_status check_async(sable_handle* h) {
   return SABLE_OK;
 }
 
+// 0 / 1: x_next is the registered fused buffer a / b; -1: not fused.
+int fused_buffer(const sable_handle* h, const void* xn) {
+  if (h->fuse_n < 0) return -1;
+  if (xn == h->fuse_buf[0]) return 0;
+  if (xn == h->fuse_buf[1]) return 1;
+  return -1;
+}
+
+void drop_fuse(sable_handle* h) {
+  for (void* b : h->fuse_ipc) cudaIpcCloseMemHandle(b);
+  h->fuse_ipc.clear();
+  h->fuse_n = -1;
+  h->fuse_buf[0] = h->fuse_buf[1] = nullptr;
+  if (h->fuse_flag) cudaFree(h->fuse_flag);
+  h->fuse_flag = nullptr;
+}
+
 // Enqueue one exchange step on st (capturable): slices compute on st and
 // their rows are broadcast on the exchange stream, which is forked from st
 // and joined back at the end.
 sable_status enqueue_step(sable_handle* h, const void* x, void* xn, cudaStream_t st) {
   const size_t sv = h->dtype == SABLE_F64 ? 8 : 4;
   char* xb = static_cast<char*>(xn);
+  const int fb = fused_buffer(h, xn);
+  if (fb >= 0) {
+    // fused epilogue: the local rows into x_next and into every peer's
+    // x_next at the same global rows, then the step barrier
+    void* peers[kMaxPeers];
+    for (int q = 0; q < h->fuse_n; ++q)
+      peers[q] = static_cast<char*>(h->fuse_peer[fb][q]) + sv * h->row_begin;
+    const cudaError_t e = run_spmv_fused(h, x, xb + sv * h->row_begin, peers, h->fuse_n, st);
+    if (e) return cuda_fail(e, "fused spmv launch");
+    if (h->comm) {
+      ncclComm_t comm = static_cast<ncclComm_t>(h->comm);
+      const ncclResult_t r = ncclAllReduce(h->fuse_flag, h->fuse_flag, 1, ncclInt32, ncclMax, comm, st);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(step barrier)");
+    }
+    return SABLE_OK;
+  }
   if (h->world == 1) {
     // one launch; SABLE_SLICED=1 runs the slice launches of the world > 1
     // pipeline back to back instead (tests: the slices tile the rows)
@@ -123,7 +170,7 @@ sable_status step_args(sable_handle* h, const void* a, const void* b, const char
     set_error(std::string(who) + ": the matrix must be square");
     return SABLE_E_DIM;
   }
-  if (h->world > 1 && !h->comm) {
+  if (h->world > 1 && !h->comm && fused_buffer(h, b) < 0) {
     set_error(std::string(who) + ": call sable_comm_init first");
     return SABLE_E_INVALID_ARG;
   }
@@ -135,6 +182,7 @@ sable_status step_args(sable_handle* h, const void* a, const void* b, const char
 sable_status comm_destroy(sable_handle* h) {
   if (!h) return SABLE_OK;
   drop_graph(h);
+  drop_fuse(h);
   if (h->comm_events) {
     for (int s = 0; s <= kSlices; ++s) cudaEventDestroy(events(h)[s]);
     delete[] events(h);
@@ -309,6 +357,157 @@ sable_status sable_spmv_iterate(sable_handle* h, void* x_a, void* x_b, int32_t i
   if (!e) e = cudaEventRecord(ev[kSlices], is);
   if (!e) e = cudaStreamWaitEvent(st, ev[kSlices], 0);
   return e ? cuda_fail(e, "iterate launch") : SABLE_OK;
+}
+
+namespace {
+
+// Register the fused buffers and their peer mappings on the handle.
+sable_status set_peers(sable_handle* h, void* x_a, void* x_b, void* const* pa, void* const* pb,
+                       int32_t n) {
+  drop_graph(h);
+  h->fuse_buf[0] = x_a;
+  h->fuse_buf[1] = x_b;
+  for (int q = 0; q < n; ++q) {
+    h->fuse_peer[0][q] = pa[q];
+    h->fuse_peer[1][q] = pb[q];
+  }
+  h->fuse_n = n;
+  if (!h->fuse_flag) {
+    cudaError_t e = cudaMalloc(&h->fuse_flag, sizeof(int32_t));
+    if (!e) e = cudaMemset(h->fuse_flag, 0, sizeof(int32_t));
+    if (e) return cuda_fail(e, "fused exchange: barrier word");
+  }
+  return SABLE_OK;
+}
+
+struct FuseMsg {  // what each rank publishes: IPC handles of the allocations
+  cudaIpcMemHandle_t mem[2];  // holding x_a / x_b, and the buffers' offsets
+  int64_t off[2];             // inside them
+};
+
+}  // namespace
+
+sable_status sable_comm_set_peers(sable_handle* h, void* x_a, void* x_b,
+                                  void* const* peers_a, void* const* peers_b, int32_t npeers) {
+  if (!h || !x_a || !x_b || x_a == x_b || npeers < 0 || npeers > kMaxPeers ||
+      (npeers > 0 && (!peers_a || !peers_b))) {
+    set_error("sable_comm_set_peers: bad arguments (two distinct buffers, 0..7 peers)");
+    return SABLE_E_INVALID_ARG;
+  }
+  for (int q = 0; q < npeers; ++q)
+    if (!peers_a[q] || !peers_b[q] || peers_a[q] == x_a || peers_b[q] == x_b) {
+      set_error("sable_comm_set_peers: NULL peer or a peer aliasing the local buffer");
+      return SABLE_E_INVALID_ARG;
+    }
+  if (h->nrows != h->ncols) {
+    set_error("sable_comm_set_peers: the matrix must be square");
+    return SABLE_E_DIM;
+  }
+  DeviceGuard g(h->device);
+  if (g.err) return cuda_fail(g.err, "sable_comm_set_peers: cudaSetDevice");
+  drop_fuse(h);
+  return set_peers(h, x_a, x_b, peers_a, peers_b, npeers);
+}
+
+sable_status sable_comm_unfuse(sable_handle* h) {
+  if (!h) {
+    set_error("sable_comm_unfuse: NULL handle");
+    return SABLE_E_INVALID_ARG;
+  }
+  DeviceGuard g(h->device);
+  if (g.err) return cuda_fail(g.err, "sable_comm_unfuse: cudaSetDevice");
+  drop_graph(h);
+  drop_fuse(h);
+  return SABLE_OK;
+}
+
+sable_status sable_comm_fuse(sable_handle* h, void* x_a, void* x_b) {
+  if (!h || !x_a || !x_b || x_a == x_b) {
+    set_error("sable_comm_fuse: two distinct device buffers required");
+    return SABLE_E_INVALID_ARG;
+  }
+  if (h->nrows != h->ncols) {
+    set_error("sable_comm_fuse: the matrix must be square");
+    return SABLE_E_DIM;
+  }
+  if (h->world > 1 && !h->comm) {
+    set_error("sable_comm_fuse: call sable_comm_init first");
+    return SABLE_E_INVALID_ARG;
+  }
+  if (h->world - 1 > kMaxPeers) {
+    set_error("sable_comm_fuse: at most 8 ranks");
+    return SABLE_E_INVALID_ARG;
+  }
+  DeviceGuard g(h->device);
+  if (g.err) return cuda_fail(g.err, "sable_comm_fuse: cudaSetDevice");
+  sable_status s = check_async(h);
+  if (s) return s;
+  drop_graph(h);
+  drop_fuse(h);
+  if (h->world == 1) return set_peers(h, x_a, x_b, nullptr, nullptr, 0);
+  // this rank's message: the IPC handle of each buffer's allocation (the
+  // driver's address range query gives its base) and the buffer's offset
+  typedef int (*range_fn)(unsigned long long*, size_t*, unsigned long long);
+  void* fp = nullptr;
+  cudaDriverEntryPointQueryResult qr;
+  cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &qr);
+  if (e || !fp || qr != cudaDriverEntryPointSuccess)
+    return cuda_fail(e ? e : cudaErrorUnknown, "sable_comm_fuse: cuMemGetAddressRange entry point");
+  FuseMsg mine;
+  void* bufs[2] = {x_a, x_b};
+  for (int i = 0; i < 2; ++i) {
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (reinterpret_cast<range_fn>(fp)(&base, &size, (unsigned long long)(uintptr_t)bufs[i]) != 0) {
+      set_error("sable_comm_fuse: x buffer is not a device allocation");
+      return SABLE_E_INVALID_ARG;
+    }
+    mine.off[i] = (int64_t)((unsigned long long)(uintptr_t)bufs[i] - base);
+    e = cudaIpcGetMemHandle(&mine.mem[i], reinterpret_cast<void*>((uintptr_t)base));
+    if (e) return cuda_fail(e, "sable_comm_fuse: cudaIpcGetMemHandle (cudaMalloc memory required)");
+  }
+  // all-gather the messages
+  const int W = h->world;
+  std::vector<FuseMsg> all((size_t)W);
+  FuseMsg* d = nullptr;
+  ncclComm_t comm = static_cast<ncclComm_t>(h->comm);
+  cudaStream_t cs = static_cast<cudaStream_t>(h->comm_stream);
+  e = cudaMalloc(&d, sizeof(FuseMsg) * (size_t)W);
+  if (!e) e = cudaMemcpyAsync(d + h->rank, &mine, sizeof(FuseMsg), cudaMemcpyHostToDevice, cs);
+  ncclResult_t r = ncclSuccess;
+  if (!e) r = ncclAllGather(d + h->rank, d, sizeof(FuseMsg), ncclInt8, comm, cs);
+  if (!e && r == ncclSuccess)
+    e = cudaMemcpyAsync(all.data(), d, sizeof(FuseMsg) * (size_t)W, cudaMemcpyDeviceToHost, cs);
+  if (!e) e = cudaStreamSynchronize(cs);
+  if (d) cudaFree(d);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather(IPC handles)");
+  if (e) return cuda_fail(e, "sable_comm_fuse: handle exchange");
+  // map every peer's two allocations (an allocation shared by both buffers
+  // is opened once)
+  void* pa[kMaxPeers];
+  void* pb[kMaxPeers];
+  int n = 0;
+  for (int q = 0; q < W; ++q) {
+    if (q == h->rank) continue;
+    void* base[2] = {nullptr, nullptr};
+    for (int i = 0; i < 2; ++i) {
+      if (i == 1 && memcmp(&all[q].mem[0], &all[q].mem[1], sizeof(cudaIpcMemHandle_t)) == 0) {
+        base[1] = base[0];
+        continue;
+      }
+      e = cudaIpcOpenMemHandle(&base[i], all[q].mem[i], cudaIpcMemLazyEnablePeerAccess);
+      if (e) {
+        drop_fuse(h);
+        return cuda_fail(e, "sable_comm_fuse: cudaIpcOpenMemHandle (one process per GPU, "
+                            "peer access over NVLink required)");
+      }
+      h->fuse_ipc.push_back(base[i]);
+    }
+    pa[n] = static_cast<char*>(base[0]) + all[q].off[0];
+    pb[n] = static_cast<char*>(base[1]) + all[q].off[1];
+    ++n;
+  }
+  return set_peers(h, x_a, x_b, pa, pb, n);
 }
 
 // The all-gather layout on the host (no GPU needed): the row bounds of every

@@ -284,6 +284,7 @@ cudaError_t run_spmm_mma(const sable_handle* h, const void* X, void* Y, int32_t 
   P.b0 = 0;
   P.n_batches = h->n_ubatch;
   P.pf = 0;
+  P.npeer = 0;
   plan_extents<float>(P, h, h->uscratch_slots * (int64_t)kM);
   int dev = 0, sms = 148;
   cudaError_t e = cudaGetDevice(&dev);

@@ -109,6 +109,7 @@ constexpr int kUnitBytes = 16384;  // default cap on one unit's data (plan.cu)
 constexpr int kBatchBytes = 8192;  // default bytes that close a warp batch (plan.cu)
 constexpr int kUnitBatch = 4;      // default units per warp batch
 constexpr int kSlices = 8;         // exchange slices of a shard (comm.cu overlap)
+constexpr int kMaxPeers = 7;       // peers of the fused exchange epilogue (world <= 8)
 
 template <typename T>
 struct UPlan {
@@ -126,6 +127,11 @@ struct UPlan {
   int32_t* counters;
   int64_t b0, n_batches;  // batches [b0, n_batches) of this launch
   int32_t pf;             // 1: bulk L2 prefetch of the next unit's data
+  // fused exchange epilogue (comm.cu): every finished y row
+  // is also stored at the same local row of npeer peer buffers (the other
+  // ranks' x_next + row_begin, reached over NVLink peer mappings)
+  int32_t npeer;
+  T* peer[kMaxPeers];
   // array extents, read only by the bounds-checked build (SABLE_CHECKED)
   int64_t n_units, pv_vecs, n_xq, n_xside, rem_nnz, nloc, ncols, n_uxg, scratch_elems;
 };
@@ -255,6 +261,13 @@ struct sable_handle {
   void* comm_stream = nullptr;       // cudaStream_t of the exchange (overlap)
   void* comm_events = nullptr;       // kSlices + 1 cudaEvent_t (slice done, exchange done)
   std::vector<int64_t> all_slice_rows;  // world * (kSlices + 1) global row bounds (host)
+  // fused exchange epilogue: the registered ping-pong buffers, the peers'
+  // mappings of the same buffers (row 0), opened IPC bases, barrier word
+  void* fuse_buf[2] = {nullptr, nullptr};
+  void* fuse_peer[2][sable::kMaxPeers] = {};
+  int32_t fuse_n = -1;               // -1: not registered; else peers per buffer
+  std::vector<void*> fuse_ipc;       // cudaIpcOpenMemHandle bases to close
+  int32_t* fuse_flag = nullptr;      // device word of the step barrier (all-reduce)
   void* graph_exec = nullptr;        // cudaGraphExec_t of sable_spmv_iterate
   const void* graph_key[2] = {nullptr, nullptr};
   int32_t graph_iters = -1;

@@ -284,9 +284,12 @@ __device__ __forceinline__ void finish_unit(const UPlan<T>& P, const Unit& U, co
                                             T* __restrict__ y, int lane) {
   if (U.xg < 0) {
     SABLE_DCHECK(U.row0 >= 0 && U.row0 + U.nr <= P.nloc);
-    if (lane < U.nr)
+    if (lane < U.nr) {
 #pragma unroll
       for (int j = 0; j < KV; ++j) y[(int64_t)(U.row0 + lane) * KV + j] = s[j];
+      if constexpr (KV == 1)  // fused exchange: the same row of every peer's x_next
+        for (int q = 0; q < P.npeer; ++q) P.peer[q][U.row0 + lane] = s[0];
+    }
     return;
   }
   const int4 gv = __ldg(reinterpret_cast<const int4*>(P.xg + U.xg));
@@ -309,6 +312,8 @@ __device__ __forceinline__ void finish_unit(const UPlan<T>& P, const Unit& U, co
         T t = __ldcg(sp + lane * KV + j);
         for (int q = 1; q < np; ++q) t += __ldcg(sp + (q * 32 + lane) * KV + j);
         y[(int64_t)(U.row0 + lane) * KV + j] = t;
+        if constexpr (KV == 1)
+          for (int q = 0; q < P.npeer; ++q) P.peer[q][U.row0 + lane] = t;
       }
     }
     if (lane == 0) P.counters[counter] = 0;  // ready for the next launch
@@ -383,6 +388,8 @@ UPlan<T> make_plan(const sable_handle* h, void* scratch) {
   P.b0 = 0;
   P.n_batches = h->n_ubatch;
   P.pf = h->cfg.pf;
+  P.npeer = 0;
+  for (int q = 0; q < kMaxPeers; ++q) P.peer[q] = nullptr;
   plan_extents<T>(P, h, 0);
   return P;
 }
@@ -390,10 +397,14 @@ UPlan<T> make_plan(const sable_handle* h, void* scratch) {
 // One launch over warp batches [b0, b1).
 template <typename T, int KV>
 cudaError_t launch_kv(const sable_handle* h, const void* x, void* y, void* scratch,
-                      cudaStream_t st, int64_t b0 = 0, int64_t b1 = -1) {
+                      cudaStream_t st, int64_t b0 = 0, int64_t b1 = -1,
+                      void* const* peers = nullptr, int npeer = 0) {
   if (b1 < 0) b1 = h->n_ubatch;
   if (b1 <= b0) return cudaSuccess;
+  if (npeer < 0 || npeer > kMaxPeers || (npeer > 0 && KV != 1)) return cudaErrorInvalidValue;
   UPlan<T> P = make_plan<T>(h, scratch);
+  P.npeer = npeer;
+  for (int q = 0; q < npeer; ++q) P.peer[q] = static_cast<T*>(peers[q]);
   P.scratch_elems = h->uscratch_slots * (scratch == h->uscratch ? 1 : KV);
   P.b0 = b0;
   P.n_batches = b1;
@@ -413,6 +424,15 @@ int32_t exec_grid(const sable_handle* h) {
 cudaError_t run_spmv(const sable_handle* h, const void* x, void* y, cudaStream_t st) {
   return h->dtype == SABLE_F64 ? launch_kv<double, 1>(h, x, y, h->uscratch, st)
                                : launch_kv<float, 1>(h, x, y, h->uscratch, st);
+}
+
+// y = A x with the fused exchange epilogue: every y row is also stored at the
+// same local row of the npeer peer buffers (comm.cu).
+cudaError_t run_spmv_fused(const sable_handle* h, const void* x, void* y, void* const* peers,
+                           int npeer, cudaStream_t st) {
+  return h->dtype == SABLE_F64
+             ? launch_kv<double, 1>(h, x, y, h->uscratch, st, 0, -1, peers, npeer)
+             : launch_kv<float, 1>(h, x, y, h->uscratch, st, 0, -1, peers, npeer);
 }
 
 // y rows of exchange slice s only (its warp batches; comm.cu).

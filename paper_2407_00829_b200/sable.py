@@ -37,7 +37,8 @@ EXPORTS = ("sable_vbr_create", "sable_spmv", "sable_spmv_host", "sable_destroy",
            "sable_spmv_iterate", "sable_status_string", "sable_last_error",
            "sable_abi_version", "sable_partition_grid", "sable_serialize",
            "sable_deserialize", "sable_spmm", "sable_comm_check", "sable_exchange_rows",
-           "sable_vbr_create_policy")
+           "sable_vbr_create_policy", "sable_comm_fuse", "sable_comm_set_peers",
+           "sable_comm_unfuse")
 
 
 class sable_vbr_desc(C.Structure):
@@ -111,6 +112,9 @@ _sig = {
     "sable_vbr_create_policy": [C.POINTER(sable_vbr_desc), C.POINTER(sable_delta_policy),
                                 C.POINTER(sable_shard), _P, C.POINTER(_H)],
     "sable_exchange_rows": [_P, C.c_int32, _P, C.c_int32, _P],
+    "sable_comm_fuse": [_H, _P, _P],
+    "sable_comm_set_peers": [_H, _P, _P, _P, _P, C.c_int32],
+    "sable_comm_unfuse": [_H],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -214,6 +218,23 @@ def sable_nccl_unique_id() -> bytes:
 def sable_comm_init(h: int, uid: bytes) -> None:
     buf = (C.c_char * 128).from_buffer_copy(uid)
     _check(_lib.sable_comm_init(_H(h), C.cast(buf, _P)), "sable_comm_init")
+
+
+def sable_comm_fuse(h: int, xa_ptr: int, xb_ptr: int) -> None:
+    _check(_lib.sable_comm_fuse(_H(h), _P(xa_ptr), _P(xb_ptr)), "sable_comm_fuse")
+
+
+def sable_comm_set_peers(h: int, xa_ptr: int, xb_ptr: int, peers_a, peers_b) -> None:
+    n = len(peers_a)
+    assert len(peers_b) == n
+    pa = (C.c_void_p * max(n, 1))(*peers_a)
+    pb = (C.c_void_p * max(n, 1))(*peers_b)
+    _check(_lib.sable_comm_set_peers(_H(h), _P(xa_ptr), _P(xb_ptr), C.cast(pa, _P),
+                                     C.cast(pb, _P), n), "sable_comm_set_peers")
+
+
+def sable_comm_unfuse(h: int) -> None:
+    _check(_lib.sable_comm_unfuse(_H(h)), "sable_comm_unfuse")
 
 
 def sable_spmv_allgather(h: int, x_ptr: int, xn_ptr: int, stream: int = 0) -> None:
@@ -391,6 +412,18 @@ class VbrMatrix:
 
     def comm_check(self):
         sable_comm_check(self.handle)
+
+    def comm_fuse(self, x_a, x_b):
+        """Register the ping-pong buffers for the fused exchange epilogue
+        (collective; plain cudaMalloc memory)."""
+        sable_comm_fuse(self.handle, x_a.data_ptr(), x_b.data_ptr())
+
+    def comm_set_peers(self, x_a, x_b, peers_a, peers_b):
+        sable_comm_set_peers(self.handle, x_a.data_ptr(), x_b.data_ptr(),
+                             [p.data_ptr() for p in peers_a], [p.data_ptr() for p in peers_b])
+
+    def comm_unfuse(self):
+        sable_comm_unfuse(self.handle)
 
     def spmv_allgather(self, x, x_next, stream=None):
         import torch

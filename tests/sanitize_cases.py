@@ -1,7 +1,8 @@
 """Small cases for compute-sanitizer runs (tests/test_gpu_sanitize.py): C1,
 random grids in fp32/fp64, long remainder rows split into pieces, tiny unit
 budgets (column chunks, many combine groups), SpMM k = 4, tensor-core SpMM
-k = 16 and 128 (fp32) and an iterated exchange step.  Exits 0 when every
+k = 16 and 128 (fp32), an iterated exchange step and the fused exchange
+epilogue with virtual ranks.  Exits 0 when every
 result matches the oracle."""
 import os
 import sys
@@ -54,6 +55,31 @@ def run(s, split="rect"):
     torch.cuda.synchronize()
 
 
+def run_fused(s, world=3):
+    """The fused exchange epilogue with `world` virtual ranks on one GPU:
+    every rank stores its rows into all the ranks' x_next."""
+    from paper_2407_00829_b200 import sable
+    arrays = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda()
+              for k, v in s.vbr_input("rect").items() if isinstance(v, np.ndarray)}
+    full = sable.VbrMatrix(arrays, s.nrows, s.ncols, delta=s.delta)
+    ranks = [sable.VbrMatrix(arrays, s.nrows, s.ncols, delta=s.delta, rank=r, world=world)
+             for r in range(world)]
+    x = torch.from_numpy(s.x).cuda()
+    xa = [x.clone() for _ in range(world)]
+    xb = [torch.empty_like(x) for _ in range(world)]
+    for r, A in enumerate(ranks):
+        o = [q for q in range(world) if q != r]
+        A.comm_set_peers(xa[r], xb[r], [xa[q] for q in o], [xb[q] for q in o])
+    for r, A in enumerate(ranks):
+        A.spmv_allgather(xa[r], xb[r])
+    want = full.spmv(x)
+    for r in range(world):
+        assert torch.equal(xb[r], want)
+    for A in ranks + [full]:
+        A.close()
+    torch.cuda.synchronize()
+
+
 def main():
     from test_gpu_parity import long_rows_synth
     cases = [gen.make("c1"), gen.make("c5", scale=1 / 512), long_rows_synth()]
@@ -62,10 +88,16 @@ def main():
                                       density=0.2, dense_cells=0.5))
     for s in cases:
         run(s)
+    for s in cases:
+        if s.nrows == s.ncols:
+            run_fused(s)
     os.environ["SABLE_USTAGE"] = "1024"  # tiny units: pieces, column chunks, combine groups
     os.environ["SABLE_UBATCH_UNITS"] = "3"
     for s in cases[1:4]:
         run(s, "all_rem")
+    for s in cases[1:4]:
+        if s.nrows == s.ncols:
+            run_fused(s, world=2)
     print("sanitize cases ok")
 
 
