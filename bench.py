@@ -7,8 +7,10 @@ nnz = true non-zeros of the whole matrix (all ranks).
 
 A step is one pass of the executor over the whole matrix, y = A x (SURVEY
 8(a) a6); with N > 1 GPUs the matrix is row-sharded (north_star s7) and a step
-is one iterated-SpMV step: local SpMV written into x_next, then the NCCL
-all-gather of the y slices (a6 + a7).  The inspector (a1..a5, sable_vbr_create)
+is one iterated-SpMV step (a6 + a7): the local SpMV written into x_next and
+its rows exchanged -- by the fused epilogue (the kernel stores each y row into
+every peer's x_next over NVLink, sable_comm_fuse; self-checked against the
+NCCL step before timing) or else by the pipelined NCCL all-gather.  The inspector (a1..a5, sable_vbr_create)
 runs once before the timed region -- compile once, run many
 -- and its time is reported as inspect_ms.
 
@@ -202,6 +204,37 @@ def run_sable(args):
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
 
+    # N > 1: the fused exchange epilogue (peer stores from the SpMV kernel,
+    # sable_comm_fuse) when every rank can map its peers and one fused step
+    # reproduces the NCCL pipeline's x_next bit for bit; else the NCCL pipeline
+    exchange, exchange_note = "none", ""
+    if world > 1:
+        exchange = "nccl"
+        ref = torch.empty_like(x)
+        A.spmv_allgather(x, ref, sp)  # unregistered buffers: the NCCL pipeline
+        ok = torch.ones(1, dtype=torch.int32, device=dev)
+        if args.exchange in ("auto", "fused"):
+            try:
+                A.comm_fuse(x, xn)
+            except sable.SableError as e:
+                ok.zero_()
+                exchange_note = str(e)
+        else:
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()):
+            A.spmv_allgather(x, xn, sp)  # xn is registered: the fused step
+            torch.cuda.synchronize()
+            ok.fill_(int(torch.equal(ref, xn)))
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()):
+                exchange = "fused"
+            else:
+                exchange_note = "fused step differed from the NCCL step (self-check): NCCL used"
+        if exchange != "fused":
+            A.comm_unfuse()
+        del ref
+
     def step():
         if world > 1:
             A.spmv_allgather(x, xn, sp)
@@ -261,7 +294,7 @@ def run_sable(args):
     e2e_ms = statistics.mean(a.elapsed_time(b) for a, b in e2e_ev)
 
     # our kernels per step: one unit-executor launch (sable::unit_kernel)
-    launches_per_step = int(info["n_unit_batches"] > 0)
+    launches_per_step = int(info["n_unit_batches"] > 0) * (8 if exchange == "nccl" else 1)
     red = torch.tensor([ms, k_ms, e2e_ms, info["bytes_alg"], kf_ms or 0.0], dtype=torch.float64,
                        device=dev)
     if world > 1:
@@ -305,7 +338,11 @@ def run_sable(args):
                 "xmap_entries": info["xmap_entries"], "exec_grid": info["exec_grid"],
                 "l2": ("flushed between timed steps (512 MiB write, then read)" if flush_l2 else
                        "not flushed: working set > 2x L2 (iterated SpMV, cache behaviour is real)"),
-                "parallelism": f"row-sharded x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+                "parallelism": f"row-sharded x{world}" + {
+                    "none": "", "nccl": " + NCCL broadcast pipeline (8 slices overlapped)",
+                    "fused": " + fused NVLink epilogue (peer stores from the SpMV kernel) + "
+                             "one-word all-reduce barrier"}[exchange],
+                **({"exchange_note": exchange_note} if exchange_note else {}),
                 "bytes_alg_per_step": info["bytes_alg"] if world == 1 else None,
             },
             "roofline": {
@@ -451,6 +488,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="sable", choices=["sable", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "fused", "nccl"],
+                    help="N > 1: fused NVLink epilogue (self-checked, falls back) or NCCL pipeline")
     ap.add_argument("--l2", default="auto", choices=["auto", "flush", "keep"],
                     help="L2 between timed steps: flush, keep, or auto (keep when the "
                          "SpMV's algorithmic bytes exceed 2x L2)")

@@ -91,6 +91,15 @@ def test_null_handles(sable):
         sable.sable_get_info(0)
     with pytest.raises(sable.SableError):
         sable.sable_spmv(0, 0, 0)
+    # the fused-exchange registration checks its arguments before any device work
+    with pytest.raises(sable.SableError) as e:
+        sable.sable_comm_fuse(0, 0, 0)
+    assert e.value.status == sable.SABLE_E_INVALID_ARG
+    with pytest.raises(sable.SableError) as e:
+        sable.sable_comm_set_peers(0, 16, 32, [], [])
+    assert e.value.status == sable.SABLE_E_INVALID_ARG
+    with pytest.raises(sable.SableError):
+        sable.sable_comm_unfuse(0)
 
 
 def brute_bounds(w, world):
