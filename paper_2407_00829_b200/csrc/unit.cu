@@ -56,12 +56,6 @@ constexpr int kUnitThreads = kUnitWarps * 32;
 #define SABLE_UNIT_MINW 32  // A/B builds: resident warps per SM asked of ptxas (64 regs)
 #endif
 constexpr int kUnitMinBlocks = SABLE_UNIT_MINW / kUnitWarps;
-#ifndef SABLE_VAL_PF
-#define SABLE_VAL_PF 0  // A/B builds: 1 = prefetch the next unit's panel rows into L2
-#endif
-#ifndef SABLE_REM_PF
-#define SABLE_REM_PF 0  // A/B builds: 1 / 2 = prefetch the first remainder wave into L1 / L2
-#endif
 
 // Lane 0: pull a warp batch's data past its first unit into L2 with five
 // bulk prefetches -- the units of a batch are consecutive, so their panel
@@ -343,26 +337,9 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
     if (lane == 0) prefetch_span<T>(P, Un, Ul);
   }
   SABLE_DCHECK(u0 >= 0 && u0 <= u1 && u1 <= P.n_units);
-#if SABLE_VAL_PF
-  // descriptors two units ahead, so that unit u + 1's panel rows can be
-  // prefetched into L2 when unit u starts
-  Unit Un2 = Un;
-  if (u0 + 1 < u1) Un2 = load_unit(P.units + u0 + 1);
-#endif
   for (int u = u0; u < u1; ++u) {
     const Unit U = Un;
-#if SABLE_VAL_PF
-    Un = Un2;
-    if (u + 2 < u1) Un2 = load_unit(P.units + u + 2);
-    if (u + 1 < u1 && Un.wq > 0) {
-      const int64_t bytes = (int64_t)Un.nr * Un.wq * 16;
-      const char* base = reinterpret_cast<const char*>(reinterpret_cast<const uint4*>(P.pv) + Un.voff16);
-      for (int64_t o = (int64_t)lane * 128; o < bytes; o += 32 * 128)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(base + o));
-    }
-#else
     if (u + 1 < u1) Un = load_unit(P.units + u + 1);
-#endif
     SABLE_DCHECK(U.nr >= 1 && U.nr <= 32 && U.llpr <= 5 && U.row0 >= 0 && U.row0 + U.nr <= P.nloc);
     SABLE_DCHECK(U.wq == 0 || (U.wq > 0 && U.voff16 >= 0 &&
                                (int64_t)U.voff16 + (int64_t)U.nr * U.wq <= P.pv_vecs &&
@@ -378,22 +355,6 @@ __global__ void __launch_bounds__(kUnitThreads, kUnitMinBlocks)
       lo = max(ldg_meta(P.rptr + U.row0 + lane), U.e0);
       hi = min(ldg_meta(P.rptr + U.row0 + lane + 1), U.e1);
     }
-#if SABLE_REM_PF
-    // the first remainder wave's columns and values towards the SM while the
-    // dense part runs: lanes 0..3 one 128-byte line of ridx each, 4..7 of rval
-    if (ne > 0 && U.wq > 0 && lane < 8) {
-      const int e = U.e0 + (lane & 3) * 32;
-      if (e < U.e1) {
-        const void* a = lane < 4 ? static_cast<const void*>(P.ridx + e)
-                                 : static_cast<const void*>(P.rval + e);
-#if SABLE_REM_PF == 1
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
-#else
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-#endif
-      }
-    }
-#endif
     if (U.wq > 0) {
       switch (U.llpr) {
         case 0: dense_rows<T, 1, KV>(P, U, x, lane, s); break;
