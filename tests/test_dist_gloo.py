@@ -116,3 +116,71 @@ def test_sharded_iteration_matches_oracle(world):
         x = y
     # column-stochastic A conserves sum(x)
     assert abs(sum(xs[-1]) - sum(xs[0])) <= 1e-9 * abs(sum(xs[0]))
+
+
+def _worker_fused(rank, world, port, out):
+    """The fused exchange protocol (KC2) over gloo: every
+    rank keeps two full ping-pong buffers; a step computes the local rows from
+    the current buffer, stores them at their global row offset into its own
+    next buffer and into every peer's next buffer (here: point-to-point sends
+    the peer places at the sender's row range -- the peer stores of the
+    kernel's epilogue), and ends with a one-word all-reduce (the barrier)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2407_00829_b200 import dist as sdist
+
+        s, area, rem_per_row = _case()
+        weights = sdist.block_row_weights(len(s.rpntr) - 1, s.rpntr, area, rem_per_row)
+        ex = sdist.sable.sable_exchange_rows(weights, s.rpntr, world)  # libsable's row layout
+        ranges = [(int(ex[q]), int(ex[q + 1])) for q in range(world)]
+        r0, r1 = ranges[rank]
+        rp = s.rowptr()
+        cur = torch.from_numpy(s.x.astype(np.float64).copy())
+        nxt = torch.full_like(cur, float("nan"))
+        xs = []
+        for k in range(3):
+            y_loc, _ = oracle.spmv_rows(rp, s.J, s.V.astype(np.float64), cur.numpy(),
+                                        np.arange(r0, r1))
+            mine = torch.from_numpy(y_loc)
+            nxt[r0:r1] = mine  # the local store
+            reqs = [dist.isend(mine, q) for q in range(world) if q != rank]  # the peer stores
+            for q in range(world):
+                if q != rank:
+                    a, b = ranges[q]
+                    dist.recv(nxt[a:b], q)  # lands at the sender's global rows
+            for r in reqs:
+                r.wait()
+            flag = torch.zeros(1, dtype=torch.int32)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)  # the step barrier
+            assert not torch.isnan(nxt).any()  # every row arrived before the barrier ended
+            xs.append(nxt.clone())
+            cur, nxt = nxt, cur
+            nxt.fill_(float("nan"))  # the buffer the next step overwrites is free
+        out.put((rank, [v.tolist() for v in xs]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_exchange_protocol(world):
+    import oracle
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pc = mp.start_processes(_worker_fused, args=(world, _free_port(), q), nprocs=world,
+                            join=False, start_method="spawn")
+    got = dict(q.get(timeout=240) for _ in range(world))
+    while not pc.join():
+        pass
+    s, _, _ = _case()
+    x = s.x.astype(np.float64)
+    for k in range(3):
+        y, sc = oracle.spmv(s.nrows, s.I, s.J, s.V.astype(np.float64), x)
+        for r in range(world):  # every rank holds the full next x after every step
+            np.testing.assert_allclose(np.asarray(got[r][k]), y, rtol=0,
+                                       atol=1e-12 * max(1.0, sc.max()))
+        assert all(got[r][k] == got[0][k] for r in range(world))  # and the same bits
+        x = y
