@@ -391,6 +391,9 @@ EXEC_CFGS = {
     "unit_mid": dict(SABLE_USTAGE=4096, SABLE_UBATCH_UNITS=7),
     # long warp batches, no L2 prefetch
     "unit_long_batches": dict(SABLE_UBATCH_UNITS=64, SABLE_XPREFETCH=0),
+    # lanes per row = the largest power of two <= the panel width (every lane busy)
+    "unit_lpr1": dict(SABLE_LPR=1),
+    "unit_lpr1_small": dict(SABLE_LPR=1, SABLE_USTAGE=2048, SABLE_UBATCH_UNITS=2),
 }
 
 
