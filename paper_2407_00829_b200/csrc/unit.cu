@@ -35,9 +35,13 @@
 //               units (very long remainder rows, very wide panels) meet in
 //               scratch and the last piece to arrive sums the pieces in piece
 //               order.
-// At the start of a warp batch (4 consecutive units) lane 0 pulls the data of
-// the batch's later units into L2 with bulk prefetches
-// (cp.async.bulk.prefetch.L2).  Every row's summation order is
+// With SABLE_XPREFETCH=1 (off by default: measured slower), lane 0 pulls the
+// data of a warp batch's later units into L2 with bulk prefetches
+// (cp.async.bulk.prefetch.L2) at the batch start.  x, the x maps and the
+// plan's metadata are loaded with an L2 evict_last policy, the panel values
+// and remainder entries evict-first.  With the fused exchange epilogue
+// (comm.cu) every finished y row is also stored into the peers' x_next.
+// Every row's summation order is
 // fixed by the matrix alone (the plan depends on the block row, never on the
 // shard count or on timing), so y is bitwise reproducible and identical for
 // every P.
